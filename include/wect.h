@@ -50,6 +50,12 @@ extern "C" {
 
 #define WECT_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define WECT_API __attribute__((visibility("default")))
+#else
+#define WECT_API
+#endif
+
 typedef enum {
   WECT_OK = 0,
   WECT_EINVAL = -1,    /* bad argument or shape */
@@ -117,7 +123,7 @@ typedef struct {
  * P:778-794).  dirs: [D, n] fp32 directions s_p (need not be unit).  out: [d_count, T]
  * of odtype: WECT_I64 for integer weights (WECT_I32 is refused: no bound), WECT_F64 for
  * float weights. */
-wect_status wect_complex(const wect_complex_desc* K, const float* dirs, int32_t D, const wect_grid* grid,
+WECT_API wect_status wect_complex(const wect_complex_desc* K, const float* dirs, int32_t D, const wect_grid* grid,
                          void* out, wect_dtype odtype, void* stream);
 
 /* WECT of a batch of uint8 images (ndim = 2, dims = {H, W}) or voxel volumes (ndim = 3,
@@ -130,35 +136,35 @@ wect_status wect_complex(const wect_complex_desc* K, const float* dirs, int32_t 
  * img: [B, dims...] uint8.  dims: HOST array.  dirs: [D, ndim] fp32.
  * out: [B, d_count, T] of WECT_I32 (refused with WECT_EOVERFLOW when
  * 255 * #cells >= 2^31) or WECT_I64. */
-wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims, const float* dirs,
+WECT_API wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims, const float* dirs,
                         int32_t D, const wect_grid* grid, void* out, wect_dtype odtype, void* stream);
 
 /* WECFs of a weighted complex for m given vertex filters (Algorithm 1 verbatim,
  * P:654-687; with unit weights the ECF).  fvals: [k0, m] fp32,
  * FVals[a, p] = f_p(v_a).  K->coords is not used.  out: [d_count, T]. */
-wect_status ecf_complex(const wect_complex_desc* K, const float* fvals, int32_t m, const wect_grid* grid,
+WECT_API wect_status ecf_complex(const wect_complex_desc* K, const float* fvals, int32_t m, const wect_grid* grid,
                         void* out, wect_dtype odtype, void* stream);
 
 /* M = max_{p, v} |<l(v), s_p>| over all k0 vertices and all D directions, in binary64
  * (P:624-628), the value wect_complex uses when grid->maxheight <= 0.  Synchronous
  * (writes *M_host).  For direction-sharded runs each rank may call this and the
  * results agree exactly. */
-wect_status wect_maxheight(const float* coords, int64_t k0, int32_t n, const float* dirs, int32_t D,
+WECT_API wect_status wect_maxheight(const float* coords, int64_t k0, int32_t n, const float* dirs, int32_t D,
                            double* M_host, void* stream);
 
 /* Synchronises `stream` and returns WECT_ERANGE if any kernel since the last call
  * recorded an out-of-range vertex index on this device (and clears the word),
  * WECT_ECUDA on a CUDA error, WECT_OK otherwise. */
-wect_status wect_sync_status(void* stream);
+WECT_API wect_status wect_sync_status(void* stream);
 
 /* Thread-local description of the last error ("" if none). */
-const char* wect_last_error(void);
+WECT_API const char* wect_last_error(void);
 
 /* Counters of the binary64 near-edge repairs since the last reset (reading A1:
  * "near-edge cases, counted and reported").  Reads synchronously. */
-wect_status wect_repair_count(uint64_t* count_host, int reset);
+WECT_API wect_status wect_repair_count(uint64_t* count_host, int reset);
 
-int32_t wect_abi_version(void);
+WECT_API int32_t wect_abi_version(void);
 
 #ifdef __cplusplus
 }

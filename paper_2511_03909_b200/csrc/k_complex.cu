@@ -1,0 +1,401 @@
+// k_complex.cu -- explicit weighted complexes (wect_complex, ecf_complex), the
+// binary64 maxheight, and the cumsum epilogue shared with the image histogram path.
+//
+// Algorithm 1 fused into one streaming pass per direction tile:
+//   line 3  VIndices = alpha(FVals)           -> per (cell, filter) in registers
+//   line 7  SimpIndices = VIndices[verts]     -> gathered heights, never materialised
+//   line 8  MSI = rmax(SimpIndices, 1)        -> max of the gathered heights (alpha is
+//                                                monotone, eq. msi)
+//   line 9  scatter_add(MSI^T, (-1)^i w)       -> shared-memory histogram, lanes = filters
+//   line 11 cumsum                             -> k_finalize (warp-shuffle scan)
+// The paper's Theta(k m) intermediates never exist: FVals for cfg4 would be
+// 41 GB of fp32.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace wect {
+
+__device__ unsigned int g_err_word = 0;
+__device__ unsigned long long g_repair_count = 0;
+
+
+// ---------------------------------------------------------------- maxheight
+// pass 1: per vertex vmax32[v] = max_p |h32(v, p)| (fp32), global max M32 and
+// R1 = max_v sum_i |x_vi| (for the guard).  pass 2 recomputes in binary64 every vertex
+// whose fp32 max is within 2 err of M32 (err bounds |h32 - h64|), so the exact M64 =
+// max |h64| is found (reading A2).
+template <int N>
+__global__ void __launch_bounds__(256) k_vmax_pass1(const float* __restrict__ coords, int64_t k0,
+                                                    const float* __restrict__ dirs, int D, float* __restrict__ vmax,
+                                                    unsigned int* __restrict__ m32_bits, unsigned int* __restrict__ r1_bits,
+                                                    unsigned int* __restrict__ smax_bits) {
+  extern __shared__ float sdir[];  // [D][N]
+  float sm = 0.f;
+  for (int i = threadIdx.x; i < D * N; i += blockDim.x) { sdir[i] = dirs[i]; sm = fmaxf(sm, fabsf(dirs[i])); }
+  if (blockIdx.x == 0) {
+    for (int o = 16; o; o >>= 1) sm = fmaxf(sm, __shfl_xor_sync(0xffffffffu, sm, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(smax_bits, __float_as_uint(sm));
+  }
+  __syncthreads();
+  float bm = 0.f, br = 0.f;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < k0; v += (int64_t)gridDim.x * blockDim.x) {
+    float x[N];
+    float r1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) { x[i] = coords[v * N + i]; r1 += fabsf(x[i]); }
+    float m = 0.f;
+    for (int p = 0; p < D; ++p) {
+      float h = x[0] * sdir[p * N];
+#pragma unroll
+      for (int i = 1; i < N; ++i) h = fmaf(x[i], sdir[p * N + i], h);
+      m = fmaxf(m, fabsf(h));
+    }
+    vmax[v] = m;
+    bm = fmaxf(bm, m);
+    br = fmaxf(br, r1);
+  }
+  for (int o = 16; o; o >>= 1) {
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    br = fmaxf(br, __shfl_xor_sync(0xffffffffu, br, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(m32_bits, __float_as_uint(bm));
+    atomicMax(r1_bits, __float_as_uint(br));
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) k_vmax_pass2(const float* __restrict__ coords, int64_t k0,
+                                                    const float* __restrict__ dirs, int D, const float* __restrict__ vmax,
+                                                    const unsigned int* __restrict__ m32_bits,
+                                                    const unsigned int* __restrict__ r1_bits,
+                                                    const unsigned int* __restrict__ smax_bits,
+                                                    unsigned long long* __restrict__ m64_bits) {
+  const float M32 = __uint_as_float(*m32_bits);
+  const float R = __uint_as_float(*r1_bits) * __uint_as_float(*smax_bits);
+  const float err = (N + 2) * kEps32 * R * 1.001f + FLT_MIN;
+  const float thresh = M32 - 2.f * err;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < k0; v += (int64_t)gridDim.x * blockDim.x) {
+    if (vmax[v] < thresh) continue;
+    double m = 0.0;
+    for (int p = 0; p < D; ++p) {
+      double h = __dmul_rn((double)coords[v * N], (double)dirs[p * N]);
+      for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)coords[v * N + i], (double)dirs[p * N + i]));
+      m = fmax(m, fabs(h));
+    }
+    atomicMax(m64_bits, dbits(m));
+  }
+}
+
+// ECF: M = max |f| over FVals (exact in fp32, so no refinement)
+__global__ void k_absmax_f32(const float* __restrict__ f, int64_t n, unsigned int* __restrict__ bits) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(f[i]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(bits, __float_as_uint(m));
+}
+
+// max |w| of integer weights (sizes the int32 shared-memory partials)
+__global__ void k_absmax_i32(const int32_t* __restrict__ w, int64_t n, unsigned int* __restrict__ out) {
+  unsigned int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int x = w[i];
+    unsigned int a = x < 0 ? 0u - (unsigned int)x : (unsigned int)x;
+    m = a > m ? a : m;
+  }
+  for (int o = 16; o; o >>= 1) { unsigned int t = __shfl_xor_sync(0xffffffffu, m, o); m = t > m ? t : m; }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// mode 0: WECT (M64 bits + R from pass 1), mode 1: ECF (M32 bits)
+__global__ void k_complex_params(int mode, int n, const unsigned long long* __restrict__ m64_bits,
+                                 const unsigned int* __restrict__ m32_bits, const unsigned int* __restrict__ r1_bits,
+                                 const unsigned int* __restrict__ smax_bits, int T, double maxheight, double lo_in, double hi_in, uint32_t flags,
+                                 GridParams* __restrict__ out) {
+  GridParams g;
+  double Mc = mode == 0 ? __longlong_as_double((long long)*m64_bits) : (double)__uint_as_float(*m32_bits);
+  double R = mode == 0 ? (double)__uint_as_float(*r1_bits) * (double)__uint_as_float(*smax_bits) * (1.0 + 1e-6) : Mc;
+  g.M = maxheight > 0 ? maxheight : Mc;
+  if (lo_in < hi_in) { g.lo = lo_in; g.hi = hi_in; } else { g.lo = -g.M; g.hi = g.M; }
+  g.T = T;
+  g.Tm1 = (double)(T - 1);
+  g.degenerate = !(g.hi > g.lo);
+  g.fp32_only = (flags & WECT_FP32_ONLY) ? 1 : 0;
+  double A = g.degenerate ? 0.0 : g.Tm1 / (g.hi - g.lo);
+  double Bc = -g.lo * A;
+  int nn = mode == 0 ? n : 0;
+  g.A = (float)A;
+  g.B = (float)Bc;
+  g.tau = (float)(2.0 * (double)kEps32 * (A * (nn + 2) * R + 2.0 * fabs(Bc) + T + 1.0));
+  g.pad = 0;
+  *out = g;
+}
+
+// ----------------------------------------------------------- index validation
+__global__ void k_check_indices(const int32_t* __restrict__ v, int64_t n, int64_t k0, unsigned int* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if ((uint32_t)v[i] >= (uint64_t)k0 || v[i] < 0) { atomicOr(flag, 1u); return; }
+}
+
+// --------------------------------------------------------------- main kernel
+// grid = (filter tiles of 32, cell slices); lanes = filters, warps = cell streams.
+// MODE 0 (WECT): h(v, p) = <coords[v], dirs[p]> (fp32 FMA fast path, binary64 repair).
+// MODE 1 (ECF):  h(v, p) = fvals[v * m + p].
+template <int MODE, int N, bool FLOATW>
+__global__ void __launch_bounds__(256) k_complex(Segs segs, const float* __restrict__ coords, int64_t k0,
+                                                 const float* __restrict__ fsrc, int m_or_D, int d_begin, int Dc,
+                                                 const GridParams* __restrict__ gp,
+                                                 const unsigned int* __restrict__ wmax_bits, int64_t slice_len,
+                                                 int64_t float_chunk, void* __restrict__ diff) {
+  using Acc = typename std::conditional<FLOATW, float, int>::type;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Acc* hist = (Acc*)smraw;  // [32][T+1]
+  __shared__ Seg ssegs[kMaxSegs];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < kMaxSegs; ++i) ssegs[i] = segs.s[i];  // constant indices: no local copy
+  }
+  const GridParams g = *gp;
+  const int T = g.T, TS = T + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int dl = blockIdx.x * 32 + lane;
+  const bool active = dl < Dc;
+  const int p = d_begin + (active ? dl : 0);
+  float s[N > 0 ? N : 1];
+  if (MODE == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) s[i] = fsrc[p * N + i];
+  }
+  const int64_t c0 = blockIdx.y * slice_len;
+  const int64_t c1 = (c0 + slice_len) < segs.total ? (c0 + slice_len) : segs.total;
+  // chunking: int32 partials must not overflow (chunk * max|w| < 2^31); float partials are
+  // flushed every float_chunk cells (reading A8 error bound)
+  int64_t chunk;
+  if (FLOATW) chunk = float_chunk;
+  else {
+    unsigned int wm = *wmax_bits;
+    chunk = wm == 0 ? c1 - c0 : (int64_t)(2147483647u / wm);
+    if (chunk < 1) chunk = 1;
+  }
+  int seg = 0;
+  for (int64_t a0 = c0; a0 < c1; a0 += chunk) {
+    const int64_t a1 = (a0 + chunk) < c1 ? (a0 + chunk) : c1;
+    for (int i = threadIdx.x; i < 32 * TS; i += blockDim.x) hist[i] = (Acc)0;
+    __syncthreads();
+    for (int64_t c = a0 + warp; c < a1; c += nwarps) {
+      while (c >= ssegs[seg].start + ssegs[seg].count) ++seg;
+      const Seg& S = ssegs[seg];
+      const int64_t b = c - S.start;
+      const int ar = S.arity;
+      float hmax = -FLT_MAX;
+      bool bad = false;
+      for (int j = 0; j < ar; ++j) {
+        int v = S.verts ? __ldg(S.verts + b * ar + j) : (int)b;
+        if ((uint64_t)(int64_t)v >= (uint64_t)k0) { bad = true; v = 0; }
+        float h;
+        if (MODE == 0) {
+          const float* x = coords + (int64_t)v * N;
+          h = __ldg(x) * s[0];
+#pragma unroll
+          for (int i = 1; i < N; ++i) h = fmaf(__ldg(x + i), s[i], h);
+        } else {
+          h = __ldg(fsrc + (int64_t)v * m_or_D + p);
+        }
+        hmax = fmaxf(hmax, h);
+      }
+      if (bad) {
+        if (lane == 0) atomicOr(&g_err_word, 1u);
+        continue;
+      }
+      int bin = alpha32_or_repair(hmax, g);
+      if (bin < 0) {
+        double hm = -DBL_MAX;
+        for (int j = 0; j < ar; ++j) {
+          const int v = S.verts ? __ldg(S.verts + b * ar + j) : (int)b;
+          double h;
+          if (MODE == 0) {
+            const float* x = coords + (int64_t)v * N;
+            h = __dmul_rn((double)x[0], (double)s[0]);
+#pragma unroll
+            for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x[i], (double)s[i]));
+          } else {
+            h = (double)fsrc[(int64_t)v * m_or_D + p];
+          }
+          hm = fmax(hm, h);
+        }
+        bin = alpha64(hm, g);
+        note_repair();
+      }
+      Acc w;
+      if (FLOATW) w = S.weights ? __ldg((const float*)S.weights + b) : 1.f;
+      else w = S.weights ? __ldg((const int*)S.weights + b) : 1;
+      if (S.sign < 0) w = -w;
+      if (active && w != (Acc)0) atomicAdd(&hist[lane * TS + bin], w);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) {
+      const int r = i / T, q = i - r * T;
+      const Acc val = hist[r * TS + q];
+      if (val != (Acc)0 && blockIdx.x * 32 + r < Dc) {
+        const int64_t o = (int64_t)(blockIdx.x * 32 + r) * T + q;
+        if (FLOATW) atomicAdd((double*)diff + o, (double)val);
+        else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ cumsum epilogue
+// Alg. 1 line 11: one warp per row, 32-wide shuffle scan with carry.
+template <typename In, typename Out>
+__global__ void k_finalize(const In* __restrict__ diff, int64_t rows, int T, Out* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const In* d = diff + row * T;
+  Out* o = out + row * T;
+  In carry = 0;
+  for (int q0 = 0; q0 < T; q0 += 32) {
+    In x = (q0 + lane < T) ? d[q0 + lane] : (In)0;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      In y = __shfl_up_sync(0xffffffffu, x, k);
+      if (lane >= k) x += y;
+    }
+    x += carry;
+    if (q0 + lane < T) o[q0 + lane] = (Out)x;
+    carry = __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+template <int MODE, int N>
+static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* coords, int64_t k0, const float* fsrc,
+                                    int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
+                                    const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
+  const int tiles = (Dc + 31) / 32;
+  const size_t smem = (size_t)32 * (T + 1) * 4;
+  // slices: >= 2 waves of CTAs, each slice <= 2^20 cells
+  int64_t total = segs.total;
+  int per_sm = (int)((220 * 1024) / (smem + 2048));
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 8) per_sm = 8;
+  int64_t want = ((int64_t)num_sms * per_sm * 2 + tiles - 1) / tiles;
+  int64_t slice = (total + want - 1) / want;
+  if (slice > ((int64_t)1 << 20)) slice = (int64_t)1 << 20;
+  if (slice < 256) slice = 256;
+  int64_t nslices = (total + slice - 1) / slice;
+  if (nslices < 1) nslices = 1;
+  dim3 grid(tiles, (unsigned)nslices);
+  const int64_t fchunk = 4096;
+  if (floatw) {
+    auto k = k_complex<MODE, N, true>;
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff);
+  } else {
+    auto k = k_complex<MODE, N, false>;
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff);
+  }
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
+                           const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
+                           const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
+  if (mode == 1) return launch_complex_n<1, 0>(floatw, segs, coords, k0, fsrc, m_or_D, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
+  switch (n) {
+#define WECT_CASE(NN) \
+  case NN: return launch_complex_n<0, NN>(floatw, segs, coords, k0, fsrc, m_or_D, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
+    WECT_CASE(1) WECT_CASE(2) WECT_CASE(3) WECT_CASE(4) WECT_CASE(5) WECT_CASE(6) WECT_CASE(7) WECT_CASE(8)
+#undef WECT_CASE
+  }
+  return fail(WECT_EINVAL, "ambient dimension n=%d outside [1,8]", n);
+}
+
+template <int N>
+static wect_status launch_vmax_n(const float* coords, int64_t k0, const float* dirs, int D, float* vmax,
+                                 unsigned int* m32, unsigned int* r1, unsigned int* smax, unsigned long long* m64,
+                                 cudaStream_t st, int num_sms) {
+  int blocks = (int)((k0 + 255) / 256);
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
+  if (blocks < 1) blocks = 1;
+  const size_t smem = (size_t)D * N * sizeof(float);
+  if (smem > 48 * 1024) WECT_CUDA_TRY(cudaFuncSetAttribute(k_vmax_pass1<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_vmax_pass1<N><<<blocks, 256, smem, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax);
+  WECT_CUDA_TRY(cudaGetLastError());
+  k_vmax_pass2<N><<<blocks, 256, 0, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax, m64);
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_vmax(int n, const float* coords, int64_t k0, const float* dirs, int D, float* vmax,
+                        unsigned int* m32, unsigned int* r1, unsigned int* smax, unsigned long long* m64, cudaStream_t st,
+                        int num_sms) {
+  switch (n) {
+#define WECT_CASE(NN) \
+  case NN: return launch_vmax_n<NN>(coords, k0, dirs, D, vmax, m32, r1, smax, m64, st, num_sms);
+    WECT_CASE(1) WECT_CASE(2) WECT_CASE(3) WECT_CASE(4) WECT_CASE(5) WECT_CASE(6) WECT_CASE(7) WECT_CASE(8)
+#undef WECT_CASE
+  }
+  return fail(WECT_EINVAL, "ambient dimension n=%d outside [1,8]", n);
+}
+
+wect_status launch_complex_params(int mode, int n, const unsigned long long* m64, const unsigned int* m32,
+                                  const unsigned int* r1, const unsigned int* smax, const wect_grid& grid,
+                                  GridParams* gp, cudaStream_t st) {
+  k_complex_params<<<1, 1, 0, st>>>(mode, n, m64, m32, r1, smax, grid.T, grid.maxheight, grid.lo, grid.hi,
+                                    grid.flags, gp);
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_absmax_f32(const float* f, int64_t n, unsigned int* bits, cudaStream_t st, int num_sms) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
+  if (blocks < 1) blocks = 1;
+  k_absmax_f32<<<blocks, 256, 0, st>>>(f, n, bits);
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_absmax_i32(const int32_t* w, int64_t n, unsigned int* out, cudaStream_t st, int num_sms) {
+  if (n <= 0) return WECT_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
+  k_absmax_i32<<<blocks, 256, 0, st>>>(w, n, out);
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_check_indices(const int32_t* v, int64_t n, int64_t k0, unsigned int* flag, cudaStream_t st,
+                                 int num_sms) {
+  if (n <= 0) return WECT_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
+  k_check_indices<<<blocks, 256, 0, st>>>(v, n, k0, flag);
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_finalize(const void* diff, bool is_float, int64_t rows, int T, void* out, wect_dtype odtype,
+                            cudaStream_t st) {
+  if (rows <= 0) return WECT_OK;
+  const int wpb = 8;
+  const unsigned blocks = (unsigned)((rows + wpb - 1) / wpb);
+  if (is_float) {
+    k_finalize<double, double><<<blocks, wpb * 32, 0, st>>>((const double*)diff, rows, T, (double*)out);
+  } else if (odtype == WECT_I32) {
+    k_finalize<long long, int><<<blocks, wpb * 32, 0, st>>>((const long long*)diff, rows, T, (int*)out);
+  } else {
+    k_finalize<long long, long long><<<blocks, wpb * 32, 0, st>>>((const long long*)diff, rows, T, (long long*)out);
+  }
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+}  // namespace wect

@@ -1,0 +1,476 @@
+// k_images.cu -- implicit image / voxel cubical complexes (wect_images).
+//
+// Cells are never listed in memory (north_star): every axis-aligned unit i-cube of
+// the pixel grid is a cell of sign (-1)^i whose weight is the max of its corners
+// (readings A5, A7).
+//
+// Exact regrouping: for a direction s, a cell's
+// height is the height of ONE designated corner -- per extended axis k, the upper
+// index when s_k > 0, else the lower -- because the height evaluation (fp32 fast
+// path and the binary64 repair alike) is monotone in each coordinate.  So per
+// direction every cell lands in the bin of its designated corner, and all cells
+// designating vertex v can be summed first into one combined weight cw_o(v), o the
+// orthant of s.  |cw| <= 255 in 2D, <= 1020 in 3D.
+//
+// Two kernels:
+//  * k_sweep2d (MNIST-shaped batches, H*W <= 1024): image-independent geometry is
+//    preprocessed once per call into, per direction, the vertices sorted by bin
+//    (counting sort, k_sort2d).  A CTA then holds 64 images' cw (biased u16, two
+//    images per 32-bit word) in shared memory and each warp sweeps one direction:
+//    lane l accumulates images 2l, 2l+1 in sorted order and emits the running sum at
+//    every bin end.  That running sum IS the cumsum of the difference histogram
+//    (Alg. 1 lines 4-11) -- no atomics, no separate scan, exact int32.
+//  * k_grid_hist (volumes, large images): lanes = 32 directions, warps stream
+//    voxels, shared-memory int32 histograms [32][T+1], one int64 merge per CTA,
+//    then k_finalize's cumsum.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace wect {
+
+// ---------------------------------------------------------------------------
+// Grid parameters: M = max |h| over the 2^ndim bounding-box corners and ALL D
+// directions (reading A2: the binary64 height is monotone per coordinate, so the
+// max over the grid is attained at a corner), plus the fp32 guard tau.
+// ---------------------------------------------------------------------------
+__global__ void k_grid_params(int ndim, int64_t d0, int64_t d1, int64_t d2, const float* __restrict__ dirs,
+                              int D, int T, double maxheight, double lo_in, double hi_in, uint32_t flags,
+                              GridParams* __restrict__ out) {
+  __shared__ double red[256];
+  __shared__ float sred[256];
+  int64_t dims[3] = {d0, d1, d2};
+  int maxd = 1;
+  for (int i = 0; i < ndim; ++i) maxd = dims[i] > maxd ? (int)dims[i] : maxd;
+  double S = (double)(maxd - 1 > 1 ? maxd - 1 : 1);
+  // axis k <-> grid dim ndim-1-k
+  float lo_c[3], hi_c[3];
+  float R1 = 0.f;
+  for (int k = 0; k < ndim; ++k) {
+    int L = (int)dims[ndim - 1 - k];
+    lo_c[k] = axis_coord(0, L, S);
+    hi_c[k] = axis_coord(L - 1, L, S);
+    R1 += fmaxf(fabsf(lo_c[k]), fabsf(hi_c[k]));
+  }
+  double M = 0.0;
+  float smax = 0.f;
+  int ncorner = 1 << ndim;
+  for (int idx = threadIdx.x; idx < D * ncorner; idx += blockDim.x) {
+    int p = idx / ncorner, c = idx % ncorner;
+    double h = 0.0;
+    for (int k = 0; k < ndim; ++k) {
+      double x = (double)(((c >> k) & 1) ? hi_c[k] : lo_c[k]);
+      double prod = __dmul_rn(x, (double)dirs[p * ndim + k]);
+      h = (k == 0) ? prod : __dadd_rn(h, prod);
+      smax = fmaxf(smax, fabsf(dirs[p * ndim + k]));
+    }
+    M = fmax(M, fabs(h));
+  }
+  red[threadIdx.x] = M;
+  sred[threadIdx.x] = smax;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+      sred[threadIdx.x] = fmaxf(sred[threadIdx.x], sred[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    GridParams g;
+    g.M = maxheight > 0 ? maxheight : red[0];
+    if (lo_in < hi_in) { g.lo = lo_in; g.hi = hi_in; } else { g.lo = -g.M; g.hi = g.M; }
+    g.T = T;
+    g.Tm1 = (double)(T - 1);
+    g.degenerate = !(g.hi > g.lo);
+    g.fp32_only = (flags & WECT_FP32_ONLY) ? 1 : 0;
+    double A = g.degenerate ? 0.0 : g.Tm1 / (g.hi - g.lo);
+    double Bc = -g.lo * A;
+    double R = (double)R1 * (double)sred[0] * (1.0 + 1e-6);
+    g.A = (float)A;
+    g.B = (float)Bc;
+    g.tau = (float)(2.0 * (double)kEps32 * (A * (ndim + 2) * R + 2.0 * fabs(Bc) + T + 1.0));
+    g.pad = 0;
+    *out = g;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per local direction: exact bins of all H*W vertices (binary64, alpha64), counting
+// sort by bin -> perm[dl][HW] (u16 vertex ids), endq[dl][q] = #{v : bin(v) <= q},
+// and the direction's quadrant o = (s_x > 0) | (s_y > 0) << 1, appended to qlist.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __restrict__ dirs, int d_begin, int Dc,
+                                                const GridParams* __restrict__ gp, uint16_t* __restrict__ perm,
+                                                uint16_t* __restrict__ endq, int* __restrict__ qlist,
+                                                int* __restrict__ qcount) {
+  extern __shared__ int sh[];  // counts[T] then cursor[T]
+  const GridParams g = *gp;
+  const int T = g.T, HW = H * W, dl = blockIdx.x, p = d_begin + dl;
+  int* counts = sh;
+  int* cursor = sh + T;
+  for (int q = threadIdx.x; q < T; q += blockDim.x) counts[q] = 0;
+  const float sx = dirs[2 * p], sy = dirs[2 * p + 1];
+  int maxd = H > W ? H : W;
+  double S = (double)(maxd - 1 > 1 ? maxd - 1 : 1);
+  __syncthreads();
+  for (int v = threadIdx.x; v < HW; v += blockDim.x) {
+    int r = v / W, c = v % W;
+    double h = __dadd_rn(__dmul_rn((double)axis_coord(c, W, S), (double)sx), __dmul_rn((double)axis_coord(r, H, S), (double)sy));
+    atomicAdd(&counts[alpha64(h, g)], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // T <= 4096 sequential prefix: negligible next to the sweep
+    int run = 0;
+    for (int q = 0; q < T; ++q) {
+      cursor[q] = run;
+      run += counts[q];
+      endq[(int64_t)dl * T + q] = (uint16_t)run;
+    }
+    int o = (sx > 0.f ? 1 : 0) | (sy > 0.f ? 2 : 0);
+    int pos = atomicAdd(&qcount[o], 1);
+    qlist[o * Dc + pos] = dl;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < HW; v += blockDim.x) {
+    int r = v / W, c = v % W;
+    double h = __dadd_rn(__dmul_rn((double)axis_coord(c, W, S), (double)sx), __dmul_rn((double)axis_coord(r, H, S), (double)sy));
+    int pos = atomicAdd(&cursor[alpha64(h, g)], 1);
+    perm[(int64_t)dl * HW + pos] = (uint16_t)v;
+  }
+}
+
+constexpr int kSweepWarps = 16;
+constexpr int kSweepImgs = 64;   // images per CTA group: lane l owns images 2l, 2l+1
+constexpr int kStageBins = 8;    // bins per staged output chunk
+constexpr int kStageStride = 68; // words per staged bin row (68 = 4 mod 32: conflict-free readout)
+constexpr int kBias = 255;       // cw in [-255, 255] -> biased u16 in [0, 510]
+constexpr int kMaxRun = 128;     // 128 * 510 < 65536: no carry between packed halves
+constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
+
+__host__ __device__ constexpr size_t sweep_pix_bytes(int HW) { return ((size_t)HW * kPixStride + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t sweep_smem_bytes(int HW) {
+  return (size_t)HW * 128 + sweep_pix_bytes(HW) + (size_t)kSweepWarps * kStageBins * kStageStride * 4;
+}
+
+template <typename OutT>
+__device__ __forceinline__ void sweep_store_chunk(const int* __restrict__ st, OutT* __restrict__ out, int64_t img0,
+                                                  int nimg, int Dc, int dl, int T, int qc, int lane) {
+  const int nb = (T - qc) < kStageBins ? (T - qc) : kStageBins;
+  if (nb == kStageBins && (T % 4) == 0) {
+    if (sizeof(OutT) == 4) {
+      // 2 lanes per image (16 B = 4 bins each), 16 images per instruction
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int m = r * 16 + (lane >> 1), j = lane & 1;
+        int4 v = make_int4(st[(4 * j + 0) * kStageStride + m], st[(4 * j + 1) * kStageStride + m],
+                           st[(4 * j + 2) * kStageStride + m], st[(4 * j + 3) * kStageStride + m]);
+        if (m < nimg) __stcs((int4*)(out + ((img0 + m) * Dc + dl) * (int64_t)T + qc + 4 * j), v);
+      }
+    } else {
+      // 4 lanes per image (16 B = 2 bins each), 8 images per instruction
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        int m = r * 8 + (lane >> 2), j = lane & 3;
+        longlong2 v = make_longlong2(st[(2 * j) * kStageStride + m], st[(2 * j + 1) * kStageStride + m]);
+        if (m < nimg) __stcs((longlong2*)(out + ((img0 + m) * Dc + dl) * (int64_t)T + qc + 2 * j), v);
+      }
+    }
+  } else {
+    for (int e = lane; e < kSweepImgs * nb; e += 32) {
+      int m = e / nb, k = e % nb;
+      if (m < nimg) out[((img0 + m) * Dc + dl) * (int64_t)T + qc + k] = (OutT)st[k * kStageStride + m];
+    }
+  }
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kSweepWarps * 32, 1)
+    k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint16_t* __restrict__ perm,
+              const uint16_t* __restrict__ endq, const int* __restrict__ qlist, const int* __restrict__ qcount,
+              int Dc, int T, OutT* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int HW = H * W;
+  uint32_t* cwb = (uint32_t*)smem;                 // [HW][32] words: images (2l, 2l+1) biased u16
+  uint8_t* pix = smem + (size_t)HW * 128;          // [HW][kPixStride] u8 (64 used)
+  int* stage = (int*)(pix + sweep_pix_bytes(HW));  // [warps][kStageBins][kStageStride]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* st = stage + warp * kStageBins * kStageStride;
+  int qc[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) qc[o] = qcount[o];
+  const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
+
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t img0 = grp * kSweepImgs;
+    const int nimg = (int)((B - img0) < kSweepImgs ? (B - img0) : kSweepImgs);
+    __syncthreads();  // the previous group's sweeps are done with pix / cwb
+    // stage the group's pixels transposed: pix[v][i]
+    for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
+      int i = f / HW, v = f - i * HW;
+      pix[v * kPixStride + i] = i < nimg ? __ldcs(img + (img0 + i) * HW + v) : (uint8_t)0;
+    }
+    for (int o = 0; o < 4; ++o) {
+      if (qc[o] == 0) continue;
+      __syncthreads();  // pix staged / previous quadrant's sweeps done with cwb
+      const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
+      for (int idx = threadIdx.x; idx < HW * 32; idx += blockDim.x) {
+        const int v = idx >> 5, l = idx & 31;
+        const int r = v / W, c = v - r * W;
+        const bool vc = (unsigned)(c + dc) < (unsigned)W, vr = (unsigned)(r + dr) < (unsigned)H;
+        const uint8_t* p0 = pix + v * kPixStride + 2 * l;
+        const uint8_t* pc = p0 + dc * kPixStride;
+        const uint8_t* pr = p0 + dr * W * kPixStride;
+        const uint8_t* pd = pr + dc * kPixStride;
+        uint32_t packed = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          int a = p0[k];
+          int cw = a;
+          int mc = 0, mr = 0;
+          if (vc) { mc = max(a, (int)pc[k]); cw -= mc; }
+          if (vr) { mr = max(a, (int)pr[k]); cw -= mr; }
+          if (vc && vr) cw += max(max(mc, mr), (int)pd[k]);
+          packed |= (uint32_t)(cw + kBias) << (16 * k);
+        }
+        cwb[v * 32 + l] = packed;
+      }
+      __syncthreads();
+      for (int k = warp; k < qc[o]; k += kSweepWarps) {
+        const int dl = qlist[o * Dc + k];
+        const uint16_t* __restrict__ P = perm + (int64_t)dl * HW;
+        const uint16_t* __restrict__ E = endq + (int64_t)dl * T;
+        int i = 0, tot0 = 0, tot1 = 0;
+        for (int q0 = 0; q0 < T; q0 += kStageBins) {
+#pragma unroll
+          for (int qq = 0; qq < kStageBins; ++qq) {
+            const int q = q0 + qq;
+            if (q < T) {
+              const int e = E[q];
+              while (i < e) {  // warp-uniform
+                const int cnt = (e - i) < kMaxRun ? (e - i) : kMaxRun;
+                uint32_t acc = 0;
+#pragma unroll 4
+                for (int t = 0; t < cnt; ++t) acc += cwb[(int)P[i + t] * 32 + lane];
+                tot0 += (int)(acc & 0xFFFFu) - kBias * cnt;
+                tot1 += (int)(acc >> 16) - kBias * cnt;
+                i += cnt;
+              }
+            }
+            *(int2*)(st + qq * kStageStride + 2 * lane) = make_int2(tot0, tot1);
+          }
+          __syncwarp();
+          sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q0, lane);
+          __syncwarp();
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Histogram path: orthant-combined weights cwo[b][v][o] (int16), o = sum_k (s_k > 0) << k.
+// cw_o(v) = sum over axis subsets A (cells anchored at v, extending one step along each
+// k in A toward -1 if bit k of o is set, else +1) of (-1)^|A| * max over the cell corners.
+// ---------------------------------------------------------------------------
+template <int ND>
+__global__ void __launch_bounds__(256) k_grid_cw(const uint8_t* __restrict__ img, int64_t nimg, int64_t d0,
+                                                 int64_t d1, int64_t d2, int16_t* __restrict__ cwo) {
+  constexpr int NO = 1 << ND;
+  int64_t L[3];  // L[k] = length of axis k (axis 0 fastest)
+  if (ND == 2) { L[0] = d1; L[1] = d0; L[2] = 1; } else { L[0] = d2; L[1] = d1; L[2] = d0; }
+  const int64_t nv = L[0] * L[1] * L[2];
+  const int64_t total = nimg * nv;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = f / nv, v = f - b * nv;
+    int64_t g[3] = {v % L[0], (v / L[0]) % L[1], v / (L[0] * L[1])};
+    const uint8_t* im = img + b * nv;
+    // 3^ND neighbourhood, -1 where outside the grid
+    int nb[ND == 2 ? 9 : 27];
+#pragma unroll
+    for (int t = 0; t < (ND == 2 ? 9 : 27); ++t) {
+      int o0 = t % 3 - 1, o1 = (t / 3) % 3 - 1, o2 = ND == 3 ? t / 9 - 1 : 0;
+      int64_t x = g[0] + o0, y = g[1] + o1, z = g[2] + o2;
+      bool ok = x >= 0 && x < L[0] && y >= 0 && y < L[1] && z >= 0 && z < L[2];
+      nb[t] = ok ? (int)im[(z * L[1] + y) * L[0] + x] : -1;
+    }
+    int16_t res[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      int cw = 0;
+#pragma unroll
+      for (int A = 0; A < NO; ++A) {
+        int m = 0;
+        bool valid = true;
+#pragma unroll
+        for (int S = 0; S < NO; ++S) {
+          if ((S & ~A) != 0) continue;  // corners = subsets of A
+          int t = 0, mul = 1;
+#pragma unroll
+          for (int k = 0; k < ND; ++k) {
+            int off = ((S >> k) & 1) ? (((o >> k) & 1) ? -1 : 1) : 0;
+            t += (off + 1) * mul;
+            mul *= 3;
+          }
+          int pv = nb[t];
+          if (pv < 0) valid = false;
+          m = pv > m ? pv : m;
+        }
+        if (valid) cw += (__popc(A) & 1) ? -m : m;
+      }
+      res[o] = (int16_t)cw;
+    }
+#pragma unroll
+    for (int o = 0; o < NO; ++o) cwo[f * NO + o] = res[o];
+  }
+}
+
+template <int ND>
+__global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ cwo, int64_t d0, int64_t d1, int64_t d2,
+                                                   const float* __restrict__ dirs, int d_begin, int Dc,
+                                                   const GridParams* __restrict__ gp, int64_t slice_len,
+                                                   int64_t b_offset, unsigned long long* __restrict__ diff) {
+  constexpr int NO = 1 << ND;
+  extern __shared__ int hist[];  // [32][T+1]
+  __shared__ float axc[3][1024];
+  const GridParams g = *gp;
+  const int T = g.T, TS = T + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int L[3];
+  if (ND == 2) { L[0] = (int)d1; L[1] = (int)d0; L[2] = 1; } else { L[0] = (int)d2; L[1] = (int)d1; L[2] = (int)d0; }
+  int maxd = L[0] > L[1] ? L[0] : L[1];
+  maxd = L[2] > maxd ? L[2] : maxd;
+  const double S = (double)(maxd - 1 > 1 ? maxd - 1 : 1);
+  for (int k = 0; k < ND; ++k)
+    for (int i = threadIdx.x; i < L[k]; i += blockDim.x) axc[k][i] = axis_coord(i, L[k], S);
+  for (int i = threadIdx.x; i < 32 * TS; i += blockDim.x) hist[i] = 0;
+  const int dl = blockIdx.x * 32 + lane;
+  const bool active = dl < Dc;
+  const int p = d_begin + (active ? dl : 0);
+  float s[3] = {0.f, 0.f, 0.f};
+  int o = 0;
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    s[k] = dirs[p * ND + k];
+    o |= (s[k] > 0.f ? 1 : 0) << k;
+  }
+  const int64_t nv = (int64_t)L[0] * L[1] * L[2];
+  const int64_t b = blockIdx.z;
+  const int64_t v0 = blockIdx.y * slice_len;
+  const int64_t v1 = (v0 + slice_len) < nv ? (v0 + slice_len) : nv;
+  __syncthreads();
+  // each warp: a contiguous run of voxels with incremental grid counters
+  const int64_t per = (v1 - v0 + nwarps - 1) / nwarps;
+  int64_t va = v0 + warp * per, vb = va + per < v1 ? va + per : v1;
+  if (va < vb) {
+    int x = (int)(va % L[0]), y = (int)((va / L[0]) % L[1]), z = (int)(va / ((int64_t)L[0] * L[1]));
+    const int16_t* cw = cwo + (b * nv) * NO;
+    for (int64_t v = va; v < vb; ++v) {
+      const float cx = axc[0][x], cy = axc[1][y];
+      float h = cx * s[0];
+      h = fmaf(cy, s[1], h);
+      float cz = 0.f;
+      if (ND == 3) { cz = axc[2][z]; h = fmaf(cz, s[2], h); }
+      int bin = alpha32_or_repair(h, g);
+      if (bin < 0) {
+        double h64 = __dadd_rn(__dmul_rn((double)cx, (double)s[0]), __dmul_rn((double)cy, (double)s[1]));
+        if (ND == 3) h64 = __dadd_rn(h64, __dmul_rn((double)cz, (double)s[2]));
+        bin = alpha64(h64, g);
+        note_repair();
+      }
+      const int w = cw[v * NO + o];
+      if (active && w != 0) atomicAdd(&hist[lane * TS + bin], w);
+      if (++x == L[0]) { x = 0; if (++y == L[1]) { y = 0; ++z; } }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) {
+    int r = i / T, q = i - r * T;
+    int val = hist[r * TS + q];
+    if (val != 0 && blockIdx.x * 32 + r < Dc)
+      atomicAdd(diff + ((b_offset + b) * Dc + blockIdx.x * 32 + r) * (int64_t)T + q, (unsigned long long)(long long)val);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers (called from api.cu)
+// ---------------------------------------------------------------------------
+wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs, int D, const wect_grid& grid,
+                               GridParams* gp, cudaStream_t st) {
+  k_grid_params<<<1, 256, 0, st>>>(ndim, dims[0], dims[1], ndim == 3 ? dims[2] : 1, dirs, D, grid.T, grid.maxheight,
+                                   grid.lo, grid.hi, grid.flags, gp);
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
+  if (ndim != 2) return false;
+  int64_t HW = dims[0] * dims[1];
+  return HW >= 1 && HW <= 1024 && T <= 65535 && sweep_smem_bytes((int)HW) <= 227 * 1024;
+}
+
+wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc,
+                           int T, const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
+                           int num_sms) {
+  const int HW = H * W;
+  uint16_t* perm = (uint16_t*)scratch;
+  uint16_t* endq = perm + (size_t)Dc * HW;
+  int* qcount = (int*)(((uintptr_t)(endq + (size_t)Dc * T) + 15) & ~(uintptr_t)15);
+  int* qlist = qcount + 4;
+  WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 4 * sizeof(int), st));
+  k_sort2d<<<Dc, 256, 2 * T * sizeof(int), st>>>(H, W, dirs, d_begin, Dc, gp, perm, endq, qlist, qcount);
+  WECT_CUDA_TRY(cudaGetLastError());
+  const size_t smem = sweep_smem_bytes(HW);
+  const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
+  const int grid = (int)(ngroups < num_sms ? ngroups : num_sms);
+  if (odtype == WECT_I32) {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_sweep2d<int32_t><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, perm, endq, qlist, qcount, Dc, T,
+                                                             (int32_t*)out);
+  } else {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_sweep2d<long long><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, perm, endq, qlist, qcount, Dc, T,
+                                                               (long long*)out);
+  }
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+size_t sweep2d_scratch_bytes(int HW, int Dc, int T) {
+  return (size_t)Dc * HW * 2 + (size_t)Dc * T * 2 + 16 + 16 + (size_t)4 * Dc * 4 + 64;
+}
+
+// histogram path over a chunk of images [b0, b0 + nb): cwo scratch for nb images, diff rows at b0
+wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndim, const int64_t* dims,
+                             const float* dirs, int d_begin, int Dc, int T, const GridParams* gp, int16_t* cwo,
+                             unsigned long long* diff, cudaStream_t st, int num_sms) {
+  const int64_t nv = ndim == 2 ? dims[0] * dims[1] : dims[0] * dims[1] * dims[2];
+  const uint8_t* im = img + b0 * nv;
+  const int64_t total = nb * nv;
+  int blocks = (int)((total + 255) / 256 < (int64_t)num_sms * 16 ? (total + 255) / 256 : (int64_t)num_sms * 16);
+  if (ndim == 2) k_grid_cw<2><<<blocks, 256, 0, st>>>(im, nb, dims[0], dims[1], 1, cwo);
+  else k_grid_cw<3><<<blocks, 256, 0, st>>>(im, nb, dims[0], dims[1], dims[2], cwo);
+  WECT_CUDA_TRY(cudaGetLastError());
+  const int tiles = (Dc + 31) / 32;
+  // slices: enough CTAs for >= 4 waves, each slice at most 2^18 voxels (int32 partials:
+  // 2^18 * 8 cells * 255 < 2^31)
+  int64_t slice = (int64_t)1 << 18;
+  int64_t want = ((int64_t)num_sms * 8 + tiles * nb - 1) / (tiles * nb);
+  if (want < 1) want = 1;
+  int64_t s2 = (nv + want - 1) / want;
+  if (s2 < slice) slice = s2 < 2048 ? 2048 : s2;
+  int64_t nslices = (nv + slice - 1) / slice;
+  const size_t smem = (size_t)32 * (T + 1) * sizeof(int);
+  dim3 gridd(tiles, (unsigned)nslices, (unsigned)nb);
+  if (ndim == 2) {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_grid_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_grid_hist<2><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], 1, dirs, d_begin, Dc, gp, slice, b0, diff);
+  } else {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_grid_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_grid_hist<3><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], dims[2], dirs, d_begin, Dc, gp, slice, b0, diff);
+  }
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+}  // namespace wect

@@ -1,0 +1,77 @@
+"""CPU-side checks of the boundary: libwect.so loads and exports every symbol that
+include/wect.h declares; the Python binding rejects bad arguments before any
+device work.  No compute calls (no GPU here)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "wect.h")).read()
+    return sorted(set(re.findall(r"WECT_API\s+[\w\s\*]+?\b(\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for n in ("wect_complex", "wect_images", "ecf_complex", "wect_maxheight", "wect_sync_status", "wect_last_error",
+              "wect_repair_count", "wect_abi_version"):
+        assert n in names
+
+
+def test_library_builds_and_exports_every_symbol():
+    from paper_2511_03909_b200 import build as b
+
+    lib = b.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (\w+)$", out, re.M))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+
+
+def test_library_loads_and_reports_version():
+    from paper_2511_03909_b200 import _lib
+
+    L = _lib.load()
+    assert L.wect_abi_version() == 1
+    for n in _lib.EXPORTS:
+        assert hasattr(L, n)
+
+
+def test_sm100a_code_present():
+    from paper_2511_03909_b200 import build as b
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", b.build()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_errors_are_synchronous():
+    """EINVAL / EOVERFLOW / ENOTSUP are returned before anything touches a device."""
+    import numpy as np
+
+    import paper_2511_03909_b200 as w
+    from paper_2511_03909_b200 import _lib
+
+    img = np.zeros((1, 4, 4), np.uint8)
+    dirs = np.zeros((3, 2), np.float32)
+    with pytest.raises(w.WectError) as e:
+        w.wect_images(img, dirs, 1)  # T < 2
+    assert e.value.status == _lib.EINVAL
+    with pytest.raises(w.WectError) as e:
+        w.wect_images(img, dirs, 8, d_begin=2, d_count=5)
+    assert e.value.status == _lib.EINVAL
+    big = np.zeros((1, 256, 256, 256), np.uint8)
+    with pytest.raises(w.WectError) as e:
+        w.wect_images(big, np.zeros((3, 3), np.float32), 8, out_dtype="int32")  # 255 * 511^3 >= 2^31
+    assert e.value.status == _lib.EOVERFLOW
+    coords = np.zeros((3, 2), np.float32)
+    cells = [(np.array([[0, 1]], np.int32), np.array([1], np.int32), 1)]
+    with pytest.raises(w.WectError) as e:
+        w.wect_complex(coords, [(np.array([[0, 1]], np.int32), None, 0)], np.zeros((2, 2), np.float32), 8)  # dim 0
+    assert e.value.status == _lib.EINVAL
+    with pytest.raises(w.WectError) as e:
+        w.wect_complex(np.zeros((3, 9), np.float32), cells, np.zeros((2, 9), np.float32), 8)  # n = 9 > 8
+    assert e.value.status == _lib.EINVAL
