@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""bench.py -- WECT throughput of the B200 hot path on BASELINE.json's configs.
+
+Default workload (N = 1 line the driver records): BASELINE.json configs[1], the
+MNIST-shaped batch -- 60,000 synthetic 28x28 uint8 images per GPU, D = 64
+directions on S^1, T = 128 bins, int32 output [60000, 64, 128].  One step = one
+wect_images call over the batch = every row of SURVEY.md section 8(a): grid M
+(a2), exact vertex bins + per-direction counting sort (a1, a3), and the sweep
+kernel (a0, a4-a7: implicit cells, max rule, signed regrouped accumulation,
+cumsum, 1.97 GB output write).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): images are sharded by batch with no data-path
+collective (weak scaling: every rank runs its own 60,000-image shard); times are the
+max over ranks (all_reduce MAX).  --impl reference times the CPU oracle (O2) on the
+host on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "WECT complexes/sec and simplex·direction updates/sec; HBM GB/s vs peak"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy, burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(key):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if key in d:
+            return d[key].get("dram_bytes_per_launch")
+    return None
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML every ~5 ms while running."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]}
+
+
+# --------------------------------------------------------------- workloads
+def workload(cfg: str, rank: int):
+    """Returns a dict describing the per-rank workload (host arrays)."""
+    if cfg in ("1", "0", "2"):
+        c = int(cfg)
+        spec = dict(synth.CONFIGS[c])
+        B, dims = spec["B"], spec["dims"]
+        seed = synth.S0 + c + 7919 * rank
+        img = synth.images_u8(B, dims, seed, "uniform" if c != 2 else "uniform")
+        n = len(dims)
+        dirs = synth.directions_s1(spec["D"]) if n == 2 else synth.directions_sphere(spec["D"], n, synth.S0 + 30)
+        nv = int(np.prod(dims))
+        ncells = int(np.prod([2 * d - 1 for d in dims]))
+        out_dtype = "int32" if 255 * ncells < 2 ** 31 else "int64"
+        osz = 4 if out_dtype == "int32" else 8
+        return dict(kind="images", name=spec["name"], img=img, dirs=dirs, T=spec["T"], B=B, out_dtype=out_dtype,
+                    units=B, updates=B * ncells * spec["D"], alg_bytes=B * nv + B * spec["D"] * spec["T"] * osz,
+                    unit="complexes/s", desc=f"{B}x{'x'.join(map(str, dims))} u8 images, D={spec['D']}, T={spec['T']}, {out_dtype} out")
+    if cfg in ("3", "4", "ecfx"):
+        c = 3 if cfg in ("3", "ecfx") else 4
+        d = synth.make_config(c)
+        cx, dirs, T = d["complex"], d["dirs"], d["T"]
+        ncells = cx.num_cells()
+        idx_bytes = sum(c_.verts.nbytes for c_ in cx.cells)
+        w_bytes = (cx.vweights.nbytes if cx.vweights is not None else 0) + sum(
+            c_.weights.nbytes for c_ in cx.cells if c_.weights is not None)
+        if cfg == "ecfx":
+            f = synth.rng(synth.S0 + 60).uniform(-1, 1, (cx.k0, 1)).astype(np.float32)
+            return dict(kind="ecf", name="ecfx_torus10M_m1", cx=cx, fvals=f, T=T, units=1, updates=ncells,
+                        alg_bytes=f.nbytes + idx_bytes + w_bytes + T * 8, unit="complexes/s",
+                        desc=f"ECF of the cfg4 torus mesh ({cx.k0} V, {ncells} cells), m=1 filter, T={T}")
+        D = dirs.shape[0]
+        return dict(kind="complex", name=d["name"], cx=cx, dirs=dirs, T=T, units=1, updates=ncells * D,
+                    alg_bytes=cx.coords.nbytes + idx_bytes + w_bytes + D * T * 8, unit="complexes/s",
+                    desc=f"explicit complex {cx.k0} V / {ncells} cells, n={cx.n}, D={D}, T={T}, "
+                         f"{'f32' if cx.is_float else 'i32'} weights")
+    raise ValueError(cfg)
+
+
+# ------------------------------------------------------------- our arm (GPU)
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2511_03909_b200 as w
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    wl = workload(args.config, rank)
+    stream = torch.cuda.current_stream(dev)
+
+    if wl["kind"] == "images":
+        img_d = torch.from_numpy(wl["img"]).to(dev)
+        dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
+        out_d = torch.empty((wl["B"], wl["dirs"].shape[0], wl["T"]),
+                            dtype=getattr(torch, wl["out_dtype"]), device=dev)
+
+        def step(flags=0):
+            w.wect_images(img_d, dirs_d, wl["T"], out_dtype=wl["out_dtype"], out=out_d, flags=flags)
+    else:
+        cx = wl["cx"]
+        cells = [(torch.from_numpy(c.verts).to(dev), None if c.weights is None else torch.from_numpy(c.weights).to(dev),
+                  c.dim) for c in cx.cells]
+        vw = None if cx.vweights is None else torch.from_numpy(cx.vweights).to(dev)
+        if wl["kind"] == "ecf":
+            f_d = torch.from_numpy(wl["fvals"]).to(dev)
+            out_d = torch.empty((1, wl["T"]), dtype=torch.float64 if cx.is_float else torch.int64, device=dev)
+
+            def step(flags=0):
+                w.ecf_complex(f_d, cells, wl["T"], vweights=vw, is_float=cx.is_float, out=out_d, flags=flags)
+        else:
+            coords_d = torch.from_numpy(cx.coords).to(dev)
+            dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
+            out_d = torch.empty((wl["dirs"].shape[0], wl["T"]), dtype=torch.float64 if cx.is_float else torch.int64,
+                                device=dev)
+
+            def step(flags=0):
+                w.wect_complex(coords_d, cells, dirs_d, wl["T"], vweights=vw, is_float=cx.is_float, out=out_d,
+                               flags=flags)
+
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(w.TIME_MAIN)
+    torch.cuda.synchronize()
+    w.sync_status()
+    w.stats(reset=True)
+    w.repair_count(reset=True)
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for i in range(K):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+            step(w.TIME_MAIN)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    w.sync_status()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    launches, tl, tms = w.stats(reset=True)
+    repairs = w.repair_count(reset=True)
+    main_ms = tms / max(tl, 1)
+    if world > 1:
+        t = torch.tensor([total_ms, main_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, main_ms = float(t[0]), float(t[1])
+
+    ms_per_step = total_ms / K
+    value = world * wl["units"] * K / (total_ms / 1e3)
+    peak, peak_src = load_peaks()
+    achieved = wl["alg_bytes"] / (main_ms / 1e3) / 1e9
+    kname = {"images": "k_sweep2d" if args.config in ("0", "1") else "k_grid_hist",
+             "complex": "k_complex", "ecf": "k_complex(ECF)"}[wl["kind"]]
+    traffic = load_traffic(f"cfg{args.config}")
+    res = {
+        "metric": METRIC,
+        "value": value,
+        "unit": wl["unit"],
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int32" if wl.get("out_dtype") == "int32" else ("f64" if wl["kind"] != "images" and wl["cx"].is_float else "int64"),
+        "data": "synthetic (seeded; DESIGN.md input recipe)",
+        "config": {"workload": wl["name"], "desc": wl["desc"], "per_gpu_units": wl["units"],
+                   "l2": f"flushed between timed steps ({flush.numel() >> 20} MiB write, untimed)",
+                   "parallelism": f"batch-sharded dp{world}" if wl["kind"] == "images" else f"replicas x{world}"},
+        "updates_per_s": world * wl["updates"] * K / (total_ms / 1e3),
+        "hbm_gbs": world * wl["alg_bytes"] * K / (total_ms / 1e3) / 1e9,
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_launch": wl["alg_bytes"], "kernel_ms": main_ms,
+                     "kernel_share_of_step": main_ms / ms_per_step},
+        "gpu_launches": int(launches),
+        "repairs_binary64": int(repairs),
+        "clocks": sampler.summary(),
+    }
+    # end to end through the public API with HOST buffers (H2D + compute + D2H every step)
+    if not args.no_e2e and wl["kind"] == "images":
+        img_h = torch.from_numpy(wl["img"]).pin_memory()
+        dirs_h = torch.from_numpy(wl["dirs"])
+        out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
+        for _ in range(2):
+            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h)
+        ke = max(1, min(5, K))
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h)
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        res["e2e"] = {"value": world * wl["units"] * ke / e2e_s, "unit": wl["unit"],
+                      "h2d_bytes_per_step": int(img_h.numel() + dirs_h.numel() * 4),
+                      "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()), "steps": ke,
+                      "path": "wect_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"}
+    elif not args.no_e2e:
+        cx = wl["cx"]
+        cells_h = [(c.verts, c.weights, c.dim) for c in cx.cells]
+        t0 = time.perf_counter()
+        ke = 2
+        for _ in range(ke):
+            if wl["kind"] == "ecf":
+                o = w.ecf_complex(wl["fvals"], cells_h, wl["T"], vweights=cx.vweights, is_float=cx.is_float)
+            else:
+                o = w.wect_complex(cx.coords, cells_h, wl["dirs"], wl["T"], vweights=cx.vweights, is_float=cx.is_float)
+        e2e_s = time.perf_counter() - t0
+        h2d = (cx.coords.nbytes if wl["kind"] != "ecf" else wl["fvals"].nbytes) + sum(
+            c.verts.nbytes + (c.weights.nbytes if c.weights is not None else 0) for c in cx.cells)
+        res["e2e"] = {"value": world * ke / e2e_s, "unit": wl["unit"], "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(o.numel() * o.element_size()), "steps": ke}
+    # the CPU oracle beside it (rank 0, N = 1 only)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
+    return res
+
+
+# ---------------------------------------------------------- the CPU oracle
+def cpu_baseline(wl, budget_s=15.0, max_units=None):
+    """Time O2 (oracle/, binary64, OpenMP over directions) on a bounded sample."""
+    import oracle
+
+    cores = oracle.num_threads()
+    if wl["kind"] == "images":
+        chunk = 500 if wl["img"].shape[1:] == (28, 28) else 1
+        done, t = 0, 0.0
+        limit = wl["B"] if max_units is None else min(max_units, wl["B"])
+        while done < limit and t < budget_s:
+            n = min(chunk, limit - done)
+            t0 = time.perf_counter()
+            oracle.wect_images(wl["img"][done:done + n], wl["dirs"], wl["T"])
+            t += time.perf_counter() - t0
+            done += n
+        return {"value": done / t, "unit": wl["unit"], "cores": cores, "kind": "oracle",
+                "sample": f"O2 on images [0, {done}) of the {wl['B']}-image workload ({t:.1f} s)"}
+    # explicit complexes: a subset of directions, scaled to complexes/s
+    import oracle as orc
+
+    cx = wl["cx"]
+    if wl["kind"] == "ecf":
+        t0 = time.perf_counter()
+        orc.ecf_complex(cx, wl["fvals"], wl["T"])
+        t = time.perf_counter() - t0
+        return {"value": 1.0 / t, "unit": wl["unit"], "cores": cores, "kind": "oracle",
+                "sample": f"O2 ECF on the full mesh ({t:.1f} s)"}
+    D = wl["dirs"].shape[0]
+    fv_time = 0.0
+    nd = 8
+    t0 = time.perf_counter()
+    orc.wect_complex(cx, wl["dirs"][:nd], wl["T"])
+    t = time.perf_counter() - t0
+    return {"value": 1.0 / (t * D / nd), "unit": wl["unit"], "cores": cores, "kind": "oracle",
+            "sample": f"O2 on {nd} of {D} directions ({t:.1f} s), scaled by D/{nd}"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, same metric/config."""
+    wl = workload(args.config, 0)
+    import oracle
+
+    per_step = 2000 if wl["kind"] == "images" else None
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if wl["kind"] == "images":
+            oracle.wect_images(wl["img"][:per_step], wl["dirs"], wl["T"])
+            units = per_step
+        else:
+            r = cpu_baseline(wl)
+            units = None
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append((dt, units, r if units is None else None))
+    if wl["kind"] == "images":
+        tot = sum(t for t, _, _ in times)
+        value = per_step * len(times) / tot
+        sample = f"O2 on images [0, {per_step}) of the {wl['B']}-image workload per step"
+    else:
+        value = statistics.median([r["value"] for _, _, r in times])
+        sample = times[0][2]["sample"]
+    cores = oracle.num_threads()
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": wl["unit"], "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(t for t, _, _ in times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 bins / int64 sums", "data": "synthetic",
+            "config": {"workload": wl["name"], "desc": wl["desc"]},
+            "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4) or ecfx")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

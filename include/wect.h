@@ -72,6 +72,8 @@ typedef enum { WECT_U8 = 1, WECT_I32 = 2, WECT_I64 = 3, WECT_F32 = 4, WECT_F64 =
 #define WECT_VALIDATE 1u   /* synchronous index pre-check before any write */
 #define WECT_FP32_ONLY 2u  /* skip the binary64 near-edge repair (experiments only; bins may then
                               differ from reading A1 for heights within rounding of a bin edge) */
+#define WECT_TIME_MAIN 4u  /* instrumentation: record CUDA events around the call's dominant kernel on
+                              `stream` (read with wect_stats); adds no synchronisation */
 
 /* One dimension i >= 1 of K: the pair (i-SimplexVertices, i-SimplexWeights) of the
  * Complex list.  verts: [count, arity] int32 row-major, values in [0, k0).
@@ -163,6 +165,11 @@ WECT_API const char* wect_last_error(void);
 /* Counters of the binary64 near-edge repairs since the last reset (reading A1:
  * "near-edge cases, counted and reported").  Reads synchronously. */
 WECT_API wect_status wect_repair_count(uint64_t* count_host, int reset);
+
+/* Instrumentation: *launches = kernels this library launched since the last reset;
+ * *timed_launches / *timed_ms = count and summed device time of the dominant-kernel launches
+ * recorded under WECT_TIME_MAIN (synchronises on their events).  reset != 0 clears all. */
+WECT_API wect_status wect_stats(uint64_t* launches, uint64_t* timed_launches, double* timed_ms, int reset);
 
 WECT_API int32_t wect_abi_version(void);
 

@@ -21,10 +21,10 @@ from typing import Iterable, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import FP32_ONLY, VALIDATE, WectError  # noqa: F401
+from ._lib import FP32_ONLY, TIME_MAIN, VALIDATE, WectError  # noqa: F401
 
 __all__ = ["wect_images", "wect_complex", "ecf_complex", "wect_maxheight", "sync_status", "repair_count",
-           "WectError", "VALIDATE", "FP32_ONLY", "load"]
+           "stats", "WectError", "VALIDATE", "FP32_ONLY", "TIME_MAIN", "load"]
 
 load = _lib.load
 
@@ -209,3 +209,12 @@ def repair_count(reset: bool = False) -> int:
     c = ctypes.c_uint64(0)
     _lib.check(L.wect_repair_count(ctypes.byref(c), 1 if reset else 0))
     return int(c.value)
+
+
+def stats(reset: bool = False):
+    """(kernel launches, timed dominant-kernel launches, their summed device ms) since the
+    last reset; the timed pair is recorded only for calls made with flags=TIME_MAIN."""
+    L = _lib.load()
+    a, b, ms = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_double(0.0)
+    _lib.check(L.wect_stats(ctypes.byref(a), ctypes.byref(b), ctypes.byref(ms), 1 if reset else 0))
+    return int(a.value), int(b.value), float(ms.value)

@@ -16,10 +16,10 @@ STATUS_NAMES = {0: "WECT_OK", -1: "WECT_EINVAL", -2: "WECT_ERANGE", -3: "WECT_EO
 # wect_dtype
 U8, I32, I64, F32, F64 = 1, 2, 3, 4, 5
 # flags
-VALIDATE, FP32_ONLY = 1, 2
+VALIDATE, FP32_ONLY, TIME_MAIN = 1, 2, 4
 
 EXPORTS = ("wect_complex", "wect_images", "ecf_complex", "wect_maxheight", "wect_sync_status", "wect_last_error",
-           "wect_repair_count", "wect_abi_version")
+           "wect_repair_count", "wect_stats", "wect_abi_version")
 
 
 class WectError(RuntimeError):
@@ -66,6 +66,9 @@ def load() -> ctypes.CDLL:
     L.wect_repair_count.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     for f in ("wect_complex", "ecf_complex", "wect_images", "wect_maxheight", "wect_sync_status", "wect_repair_count"):
         getattr(L, f).restype = ctypes.c_int
+    L.wect_stats.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                             ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    L.wect_stats.restype = ctypes.c_int
     L.wect_abi_version.restype = ctypes.c_int32
     _L = L
     return L

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -27,6 +28,33 @@ wect_status fail_cuda(cudaError_t e, const char* what, const char* file, int lin
            what, file, line);
   return e == cudaErrorMemoryAllocation ? WECT_ENOMEM : WECT_ECUDA;
 }
+
+// --------------------------------------------------------- instrumentation
+static std::atomic<uint64_t> g_launches{0};
+thread_local bool t_time_main = false;
+static std::mutex g_tmu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timed;
+
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+MainTimer::MainTimer(cudaStream_t s) : st(s) {
+  if (!t_time_main) return;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
+  cudaEventRecord(a, st);
+}
+void MainTimer::stop() {
+  if (!a) return;
+  cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timed.emplace_back(a, b);
+  a = b = nullptr;
+}
+
+// RAII: instrumentation flag for the duration of one API call
+struct TimeScope {
+  explicit TimeScope(uint32_t flags) { t_time_main = (flags & WECT_TIME_MAIN) != 0; }
+  ~TimeScope() { t_time_main = false; }
+};
 
 // ------------------------------------------------------------- launchers
 wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs, int D, const wect_grid& grid,
@@ -158,6 +186,38 @@ extern "C" {
 
 int32_t wect_abi_version(void) { return WECT_ABI_VERSION; }
 
+wect_status wect_stats(uint64_t* launches, uint64_t* timed_launches, double* timed_ms, int reset) {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    ev.swap(g_timed);
+  }
+  double ms = 0.0;
+  for (auto& e : ev) {
+    float t = 0.f;
+    WECT_CUDA_TRY(cudaEventSynchronize(e.second));
+    WECT_CUDA_TRY(cudaEventElapsedTime(&t, e.first, e.second));
+    ms += t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  static double acc_ms = 0.0;
+  static uint64_t acc_n = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  acc_ms += ms;
+  acc_n += ev.size();
+  if (launches) *launches = g_launches.load();
+  if (timed_launches) *timed_launches = acc_n;
+  if (timed_ms) *timed_ms = acc_ms;
+  if (reset) {
+    acc_ms = 0.0;
+    acc_n = 0;
+    g_launches.store(0);
+  }
+  return WECT_OK;
+}
+
 const char* wect_last_error(void) { return g_msg; }
 
 wect_status wect_sync_status(void* stream) {
@@ -188,6 +248,7 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   g_msg[0] = 0;
   cudaStream_t st = (cudaStream_t)stream;
   if (!grid) return fail(WECT_EINVAL, "grid is NULL");
+  TimeScope ts(grid->flags);
   if (ndim != 2 && ndim != 3) return fail(WECT_EINVAL, "ndim must be 2 or 3 (got %d)", ndim);
   if (!dims) return fail(WECT_EINVAL, "dims is NULL");
   if (B < 0) return fail(WECT_EINVAL, "B < 0");
@@ -276,6 +337,7 @@ static wect_status run_complex(int mode, const wect_complex_desc* K, const float
   wect_status s = validate_complex(K, mode == 0);
   if (s != WECT_OK) return s;
   if (!grid) return fail(WECT_EINVAL, "grid is NULL");
+  TimeScope ts(grid->flags);
   if (grid->T < 2) return fail(WECT_EINVAL, "T must be >= 2 (beta divides by T-1)");
   if (grid->T > 4096) return fail(WECT_ENOTSUP, "T > 4096 not supported");
   if (D < 1) return fail(WECT_EINVAL, mode == 0 ? "need D >= 1 directions" : "need m >= 1 filters");

@@ -101,6 +101,15 @@ __device__ __forceinline__ float axis_coord(int g, int L, double S) {
   } while (0)
 
 namespace wect {
+// instrumentation (api.cu): kernel launch counter and optional dominant-kernel events
+void count_launch(int n = 1);
+extern thread_local bool t_time_main;
+struct MainTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  explicit MainTimer(cudaStream_t s);
+  void stop();
+};
 wect_status fail_cuda(cudaError_t e, const char* what, const char* file, int line);
 wect_status fail(wect_status s, const char* fmt, ...);
 }  // namespace wect

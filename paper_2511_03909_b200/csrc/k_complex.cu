@@ -291,15 +291,17 @@ static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* 
   if (nslices < 1) nslices = 1;
   dim3 grid(tiles, (unsigned)nslices);
   const int64_t fchunk = 4096;
+  MainTimer timer(st);
   if (floatw) {
     auto k = k_complex<MODE, N, true>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff);
+    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff); count_launch();
   } else {
     auto k = k_complex<MODE, N, false>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff);
+    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff); count_launch();
   }
+  timer.stop();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -326,9 +328,9 @@ static wect_status launch_vmax_n(const float* coords, int64_t k0, const float* d
   if (blocks < 1) blocks = 1;
   const size_t smem = (size_t)D * N * sizeof(float);
   if (smem > 48 * 1024) WECT_CUDA_TRY(cudaFuncSetAttribute(k_vmax_pass1<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_vmax_pass1<N><<<blocks, 256, smem, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax);
+  k_vmax_pass1<N><<<blocks, 256, smem, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
-  k_vmax_pass2<N><<<blocks, 256, 0, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax, m64);
+  k_vmax_pass2<N><<<blocks, 256, 0, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax, m64); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -349,7 +351,7 @@ wect_status launch_complex_params(int mode, int n, const unsigned long long* m64
                                   const unsigned int* r1, const unsigned int* smax, const wect_grid& grid,
                                   GridParams* gp, cudaStream_t st) {
   k_complex_params<<<1, 1, 0, st>>>(mode, n, m64, m32, r1, smax, grid.T, grid.maxheight, grid.lo, grid.hi,
-                                    grid.flags, gp);
+                                    grid.flags, gp); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -358,7 +360,7 @@ wect_status launch_absmax_f32(const float* f, int64_t n, unsigned int* bits, cud
   int blocks = (int)((n + 255) / 256);
   if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (blocks < 1) blocks = 1;
-  k_absmax_f32<<<blocks, 256, 0, st>>>(f, n, bits);
+  k_absmax_f32<<<blocks, 256, 0, st>>>(f, n, bits); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -367,7 +369,7 @@ wect_status launch_absmax_i32(const int32_t* w, int64_t n, unsigned int* out, cu
   if (n <= 0) return WECT_OK;
   int blocks = (int)((n + 255) / 256);
   if (blocks > num_sms * 8) blocks = num_sms * 8;
-  k_absmax_i32<<<blocks, 256, 0, st>>>(w, n, out);
+  k_absmax_i32<<<blocks, 256, 0, st>>>(w, n, out); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -377,7 +379,7 @@ wect_status launch_check_indices(const int32_t* v, int64_t n, int64_t k0, unsign
   if (n <= 0) return WECT_OK;
   int blocks = (int)((n + 255) / 256);
   if (blocks > num_sms * 8) blocks = num_sms * 8;
-  k_check_indices<<<blocks, 256, 0, st>>>(v, n, k0, flag);
+  k_check_indices<<<blocks, 256, 0, st>>>(v, n, k0, flag); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -388,11 +390,11 @@ wect_status launch_finalize(const void* diff, bool is_float, int64_t rows, int T
   const int wpb = 8;
   const unsigned blocks = (unsigned)((rows + wpb - 1) / wpb);
   if (is_float) {
-    k_finalize<double, double><<<blocks, wpb * 32, 0, st>>>((const double*)diff, rows, T, (double*)out);
+    k_finalize<double, double><<<blocks, wpb * 32, 0, st>>>((const double*)diff, rows, T, (double*)out); count_launch();
   } else if (odtype == WECT_I32) {
-    k_finalize<long long, int><<<blocks, wpb * 32, 0, st>>>((const long long*)diff, rows, T, (int*)out);
+    k_finalize<long long, int><<<blocks, wpb * 32, 0, st>>>((const long long*)diff, rows, T, (int*)out); count_launch();
   } else {
-    k_finalize<long long, long long><<<blocks, wpb * 32, 0, st>>>((const long long*)diff, rows, T, (long long*)out);
+    k_finalize<long long, long long><<<blocks, wpb * 32, 0, st>>>((const long long*)diff, rows, T, (long long*)out); count_launch();
   }
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;

@@ -148,9 +148,14 @@ constexpr int kBias = 255;       // cw in [-255, 255] -> biased u16 in [0, 510]
 constexpr int kMaxRun = 128;     // 128 * 510 < 65536: no carry between packed halves
 constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
 
-__host__ __device__ constexpr size_t sweep_pix_bytes(int HW) { return ((size_t)HW * kPixStride + 15) & ~(size_t)15; }
-__host__ __device__ constexpr size_t sweep_smem_bytes(int HW) {
-  return (size_t)HW * 128 + sweep_pix_bytes(HW) + (size_t)kSweepWarps * kStageBins * kStageStride * 4;
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t sweep_pix_bytes(int HW) { return align16((size_t)HW * kPixStride); }
+// per-warp private area: its direction's sorted vertex ids and bin ends, and the output stage
+__host__ __device__ constexpr size_t sweep_warp_bytes(int HW, int T) {
+  return align16((size_t)HW * 2) + align16((size_t)T * 2) + (size_t)kStageBins * kStageStride * 4;
+}
+__host__ __device__ constexpr size_t sweep_smem_bytes(int HW, int T) {
+  return (size_t)HW * 128 + sweep_pix_bytes(HW) + (size_t)kSweepWarps * sweep_warp_bytes(HW, T);
 }
 
 template <typename OutT>
@@ -184,6 +189,49 @@ __device__ __forceinline__ void sweep_store_chunk(const int* __restrict__ st, Ou
   }
 }
 
+// One warp, one direction, the CTA's 64 images: walk the vertices in bin order and emit
+// the running (cumulative) sum at every bin end.  sid: this direction's vertex ids in
+// bin order (warp-private smem copy); send: send[q] = #{v : bin(v) <= q}.
+template <typename OutT>
+__device__ __forceinline__ void sweep_direction(const uint32_t* __restrict__ cwb_lane, const uint16_t* __restrict__ sid,
+                                                const uint16_t* __restrict__ send, int* __restrict__ st,
+                                                OutT* __restrict__ out, int64_t img0, int nimg, int Dc, int dl, int T,
+                                                int lane) {
+  int i = 0, tot0 = 0, tot1 = 0;
+  for (int q0 = 0; q0 < T; q0 += kStageBins) {
+    const int qn = (T - q0) < kStageBins ? (T - q0) : kStageBins;
+    for (int qq = 0; qq < qn; ++qq) {
+      const int e = send[q0 + qq];
+      while (i < e) {  // warp-uniform run [i, e) of vertices in bin q0 + qq
+        const int cnt = (e - i) < kMaxRun ? (e - i) : kMaxRun;
+        const int stop = i + cnt;
+        uint32_t a = 0, b = 0;
+        int t = i;
+        switch (cnt & 3) {  // remainder first, then groups of 4 (independent loads)
+          case 3: a += cwb_lane[(uint32_t)sid[t++] * 32];  // fallthrough
+          case 2: b += cwb_lane[(uint32_t)sid[t++] * 32];  // fallthrough
+          case 1: a += cwb_lane[(uint32_t)sid[t++] * 32];  // fallthrough
+          default: break;
+        }
+#pragma unroll 1
+        for (; t < stop; t += 4) {
+          const uint32_t v0 = sid[t], v1 = sid[t + 1], v2 = sid[t + 2], v3 = sid[t + 3];
+          a += cwb_lane[v0 * 32] + cwb_lane[v1 * 32];
+          b += cwb_lane[v2 * 32] + cwb_lane[v3 * 32];
+        }
+        a += b;
+        tot0 += (int)(a & 0xFFFFu) - kBias * cnt;
+        tot1 += (int)(a >> 16) - kBias * cnt;
+        i = stop;
+      }
+      *(int2*)(st + qq * kStageStride + 2 * lane) = make_int2(tot0, tot1);
+    }
+    __syncwarp();
+    sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q0, lane);
+    __syncwarp();
+  }
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(kSweepWarps * 32, 1)
     k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint16_t* __restrict__ perm,
@@ -193,76 +241,79 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   const int HW = H * W;
   uint32_t* cwb = (uint32_t*)smem;                 // [HW][32] words: images (2l, 2l+1) biased u16
   uint8_t* pix = smem + (size_t)HW * 128;          // [HW][kPixStride] u8 (64 used)
-  int* stage = (int*)(pix + sweep_pix_bytes(HW));  // [warps][kStageBins][kStageStride]
+  unsigned char* wbase = pix + sweep_pix_bytes(HW) + (size_t)(threadIdx.x >> 5) * sweep_warp_bytes(HW, T);
+  uint16_t* sid = (uint16_t*)wbase;                               // [HW]
+  uint16_t* send = (uint16_t*)(wbase + align16((size_t)HW * 2));  // [T]
+  int* st = (int*)(wbase + align16((size_t)HW * 2) + align16((size_t)T * 2));  // [kStageBins][kStageStride]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int* st = stage + warp * kStageBins * kStageStride;
-  int qc[4];
-#pragma unroll
-  for (int o = 0; o < 4; ++o) qc[o] = qcount[o];
+  const uint32_t* cwb_lane = cwb + lane;
+  const int qc0 = qcount[0], qc1 = qcount[1], qc2 = qcount[2], qc3 = qcount[3];
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
 
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t img0 = grp * kSweepImgs;
     const int nimg = (int)((B - img0) < kSweepImgs ? (B - img0) : kSweepImgs);
     __syncthreads();  // the previous group's sweeps are done with pix / cwb
-    // stage the group's pixels transposed: pix[v][i]
-    for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
-      int i = f / HW, v = f - i * HW;
-      pix[v * kPixStride + i] = i < nimg ? __ldcs(img + (img0 + i) * HW + v) : (uint8_t)0;
+    // stage the group's pixels transposed: pix[v][i] (16-byte global loads when aligned)
+    if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
+      const int per = HW >> 4;
+      for (int f = threadIdx.x; f < kSweepImgs * per; f += blockDim.x) {
+        const int i = f / per, v = (f - i * per) << 4;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (i < nimg) x = __ldcs((const uint4*)(img + (img0 + i) * HW + v));
+        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pix[(v + k) * kPixStride + i] = (uint8_t)(wv[k >> 2] >> (8 * (k & 3)));
+      }
+    } else {
+      for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
+        const int i = f / HW, v = f - i * HW;
+        pix[v * kPixStride + i] = i < nimg ? __ldcs(img + (img0 + i) * HW + v) : (uint8_t)0;
+      }
     }
+#pragma unroll 1
     for (int o = 0; o < 4; ++o) {
-      if (qc[o] == 0) continue;
+      const int qco = o == 0 ? qc0 : (o == 1 ? qc1 : (o == 2 ? qc2 : qc3));
+      if (qco == 0) continue;
       __syncthreads();  // pix staged / previous quadrant's sweeps done with cwb
       const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
-      for (int idx = threadIdx.x; idx < HW * 32; idx += blockDim.x) {
-        const int v = idx >> 5, l = idx & 31;
-        const int r = v / W, c = v - r * W;
-        const bool vc = (unsigned)(c + dc) < (unsigned)W, vr = (unsigned)(r + dr) < (unsigned)H;
-        const uint8_t* p0 = pix + v * kPixStride + 2 * l;
-        const uint8_t* pc = p0 + dc * kPixStride;
-        const uint8_t* pr = p0 + dr * W * kPixStride;
-        const uint8_t* pd = pr + dc * kPixStride;
-        uint32_t packed = 0;
+      {
+        // element (v, l): v advances by 16 per iteration (512 threads / 32 lanes)
+        const int l = lane;
+        int v = threadIdx.x >> 5;
+        int r = v / W, c = v - r * W;
+        const int step_r = 16 / W, step_c = 16 - step_r * W;
+        for (; v < HW; v += 16) {
+          const bool vc = (unsigned)(c + dc) < (unsigned)W, vr = (unsigned)(r + dr) < (unsigned)H;
+          const uint8_t* p0 = pix + v * kPixStride + 2 * l;
+          const uint32_t a2 = *(const uint16_t*)p0;
+          uint32_t packed = 0;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          int a = p0[k];
-          int cw = a;
-          int mc = 0, mr = 0;
-          if (vc) { mc = max(a, (int)pc[k]); cw -= mc; }
-          if (vr) { mr = max(a, (int)pr[k]); cw -= mr; }
-          if (vc && vr) cw += max(max(mc, mr), (int)pd[k]);
-          packed |= (uint32_t)(cw + kBias) << (16 * k);
+          for (int k = 0; k < 2; ++k) {
+            const int a = (a2 >> (8 * k)) & 0xFF;
+            int cw = a, mc = 0, mr = 0;
+            if (vc) { mc = max(a, (int)p0[dc * kPixStride + k]); cw -= mc; }
+            if (vr) { mr = max(a, (int)p0[dr * W * kPixStride + k]); cw -= mr; }
+            if (vc && vr) cw += max(max(mc, mr), (int)p0[(dr * W + dc) * kPixStride + k]);
+            packed |= (uint32_t)(cw + kBias) << (16 * k);
+          }
+          cwb[v * 32 + l] = packed;
+          r += step_r;
+          c += step_c;
+          if (c >= W) { c -= W; ++r; }
         }
-        cwb[v * 32 + l] = packed;
       }
       __syncthreads();
-      for (int k = warp; k < qc[o]; k += kSweepWarps) {
+      for (int k = warp; k < qco; k += kSweepWarps) {
         const int dl = qlist[o * Dc + k];
-        const uint16_t* __restrict__ P = perm + (int64_t)dl * HW;
-        const uint16_t* __restrict__ E = endq + (int64_t)dl * T;
-        int i = 0, tot0 = 0, tot1 = 0;
-        for (int q0 = 0; q0 < T; q0 += kStageBins) {
-#pragma unroll
-          for (int qq = 0; qq < kStageBins; ++qq) {
-            const int q = q0 + qq;
-            if (q < T) {
-              const int e = E[q];
-              while (i < e) {  // warp-uniform
-                const int cnt = (e - i) < kMaxRun ? (e - i) : kMaxRun;
-                uint32_t acc = 0;
-#pragma unroll 4
-                for (int t = 0; t < cnt; ++t) acc += cwb[(int)P[i + t] * 32 + lane];
-                tot0 += (int)(acc & 0xFFFFu) - kBias * cnt;
-                tot1 += (int)(acc >> 16) - kBias * cnt;
-                i += cnt;
-              }
-            }
-            *(int2*)(st + qq * kStageStride + 2 * lane) = make_int2(tot0, tot1);
-          }
-          __syncwarp();
-          sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q0, lane);
-          __syncwarp();
-        }
+        // warp-private copies of this direction's tables
+        const uint16_t* P = perm + (int64_t)dl * HW;
+        const uint16_t* E = endq + (int64_t)dl * T;
+        for (int t = lane; t < HW; t += 32) sid[t] = P[t];
+        for (int t = lane; t < T; t += 32) send[t] = E[t];
+        __syncwarp();
+        sweep_direction<OutT>(cwb_lane, sid, send, st, out, img0, nimg, Dc, dl, T, lane);
+        __syncwarp();
       }
     }
   }
@@ -398,7 +449,7 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
 wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs, int D, const wect_grid& grid,
                                GridParams* gp, cudaStream_t st) {
   k_grid_params<<<1, 256, 0, st>>>(ndim, dims[0], dims[1], ndim == 3 ? dims[2] : 1, dirs, D, grid.T, grid.maxheight,
-                                   grid.lo, grid.hi, grid.flags, gp);
+                                   grid.lo, grid.hi, grid.flags, gp); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -406,7 +457,7 @@ wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs,
 bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
   if (ndim != 2) return false;
   int64_t HW = dims[0] * dims[1];
-  return HW >= 1 && HW <= 1024 && T <= 65535 && sweep_smem_bytes((int)HW) <= 227 * 1024;
+  return HW >= 1 && HW <= 1024 && T <= 65535 && sweep_smem_bytes((int)HW, T) <= 227 * 1024;
 }
 
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc,
@@ -418,20 +469,22 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   int* qcount = (int*)(((uintptr_t)(endq + (size_t)Dc * T) + 15) & ~(uintptr_t)15);
   int* qlist = qcount + 4;
   WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 4 * sizeof(int), st));
-  k_sort2d<<<Dc, 256, 2 * T * sizeof(int), st>>>(H, W, dirs, d_begin, Dc, gp, perm, endq, qlist, qcount);
+  k_sort2d<<<Dc, 256, 2 * T * sizeof(int), st>>>(H, W, dirs, d_begin, Dc, gp, perm, endq, qlist, qcount); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
-  const size_t smem = sweep_smem_bytes(HW);
+  const size_t smem = sweep_smem_bytes(HW, T);
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
   const int grid = (int)(ngroups < num_sms ? ngroups : num_sms);
+  MainTimer timer(st);
   if (odtype == WECT_I32) {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_sweep2d<int32_t><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, perm, endq, qlist, qcount, Dc, T,
-                                                             (int32_t*)out);
+                                                             (int32_t*)out); count_launch();
   } else {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_sweep2d<long long><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, perm, endq, qlist, qcount, Dc, T,
-                                                               (long long*)out);
+                                                               (long long*)out); count_launch();
   }
+  timer.stop();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
@@ -450,6 +503,7 @@ wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndi
   int blocks = (int)((total + 255) / 256 < (int64_t)num_sms * 16 ? (total + 255) / 256 : (int64_t)num_sms * 16);
   if (ndim == 2) k_grid_cw<2><<<blocks, 256, 0, st>>>(im, nb, dims[0], dims[1], 1, cwo);
   else k_grid_cw<3><<<blocks, 256, 0, st>>>(im, nb, dims[0], dims[1], dims[2], cwo);
+  count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   const int tiles = (Dc + 31) / 32;
   // slices: enough CTAs for >= 4 waves, each slice at most 2^18 voxels (int32 partials:
@@ -462,13 +516,15 @@ wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndi
   int64_t nslices = (nv + slice - 1) / slice;
   const size_t smem = (size_t)32 * (T + 1) * sizeof(int);
   dim3 gridd(tiles, (unsigned)nslices, (unsigned)nb);
+  MainTimer timer(st);
   if (ndim == 2) {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_grid_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_grid_hist<2><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], 1, dirs, d_begin, Dc, gp, slice, b0, diff);
+    k_grid_hist<2><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], 1, dirs, d_begin, Dc, gp, slice, b0, diff); count_launch();
   } else {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_grid_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_grid_hist<3><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], dims[2], dirs, d_begin, Dc, gp, slice, b0, diff);
+    k_grid_hist<3><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], dims[2], dirs, d_begin, Dc, gp, slice, b0, diff); count_launch();
   }
+  timer.stop();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
