@@ -97,19 +97,47 @@ __global__ void k_grid_params(int ndim, int64_t d0, int64_t d1, int64_t d2, cons
 
 // ---------------------------------------------------------------------------
 // Per local direction: exact bins of all H*W vertices (binary64, alpha64), counting
-// sort by bin -> perm[dl][HW] (u16 vertex ids), endq[dl][q] = #{v : bin(v) <= q},
-// and the direction's quadrant o = (s_x > 0) | (s_y > 0) << 1, appended to qlist.
+// sort by bin, and the direction's SWEEP PROGRAM:
+//   off[k]  : packets of four u32 byte offsets (id * 128) into the cw table, k < npk;
+//             each bin's ids are padded to whole packets with the padding row HW
+//             (whose packed value is the bias, i.e. weight 0)
+//   mask[k/32] bit k%32 : packet k ends a chunk (fold the packed sums into the totals)
+//   emit[i] : for the i-th flagged packet, the number of bins whose value is the running
+//             total after it (bin q with z empty bins after it emits 1 + z; chunk splits
+//             of bins with > kMaxRun ids emit 0; leading empty bins ride on an
+//             all-padding packet)
+// Layout per direction (u32 words): [off: 4*Lp][mask: Lp/32+1][emit: Lp (u16, padded)].
+// Also records the direction's quadrant o = (s_x > 0) | (s_y > 0) << 1 in qlist.
 // ---------------------------------------------------------------------------
+constexpr int kMaxRun = 128;     // ids per chunk: 128 * 510 < 65536, no carry between packed halves
+
+__host__ __device__ constexpr int sweep_prog_packets(int HW, int T) { return (HW / 4 + T + 12) & ~3; }
+__host__ __device__ constexpr int sweep_mask_words(int HW, int T) { return sweep_prog_packets(HW, T) / 32 + 1; }
+// u32 words per direction program
+__host__ __device__ constexpr int sweep_prog_words(int HW, int T) {
+  return (4 * sweep_prog_packets(HW, T) + sweep_mask_words(HW, T) + (sweep_prog_packets(HW, T) + 1) / 2 + 4 + 3) & ~3;
+}
+
 __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __restrict__ dirs, int d_begin, int Dc,
-                                                const GridParams* __restrict__ gp, uint16_t* __restrict__ perm,
-                                                uint16_t* __restrict__ endq, int* __restrict__ qlist,
+                                                const GridParams* __restrict__ gp, uint32_t* __restrict__ prog,
+                                                int* __restrict__ prog_len, int* __restrict__ qlist,
                                                 int* __restrict__ qcount) {
-  extern __shared__ int sh[];  // counts[T] then cursor[T]
+  // smem: counts[T], base[T], meta[Lp] (emit | flag << 16), vbin[HW] (u16)
+  extern __shared__ int sh[];
   const GridParams g = *gp;
   const int T = g.T, HW = H * W, dl = blockIdx.x, p = d_begin + dl;
+  const int Lp = sweep_prog_packets(HW, T);
   int* counts = sh;
-  int* cursor = sh + T;
+  int* base = sh + T;
+  int* meta = sh + 2 * T;
+  uint16_t* vbin = (uint16_t*)(sh + 2 * T + Lp);
+  __shared__ int npk_total;
+  uint32_t* off = prog + (int64_t)dl * sweep_prog_words(HW, T);
+  uint32_t* mask = off + 4 * Lp;
+  uint16_t* emitv = (uint16_t*)(mask + sweep_mask_words(HW, T));
   for (int q = threadIdx.x; q < T; q += blockDim.x) counts[q] = 0;
+  for (int k = threadIdx.x; k < Lp; k += blockDim.x) meta[k] = 0;
+  for (int k = threadIdx.x; k < 4 * Lp; k += blockDim.x) off[k] = (uint32_t)HW * 128u;  // padding row
   const float sx = dirs[2 * p], sy = dirs[2 * p + 1];
   int maxd = H > W ? H : W;
   double S = (double)(maxd - 1 > 1 ? maxd - 1 : 1);
@@ -117,26 +145,51 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
   for (int v = threadIdx.x; v < HW; v += blockDim.x) {
     int r = v / W, c = v % W;
     double h = __dadd_rn(__dmul_rn((double)axis_coord(c, W, S), (double)sx), __dmul_rn((double)axis_coord(r, H, S), (double)sy));
-    atomicAdd(&counts[alpha64(h, g)], 1);
+    int bq = alpha64(h, g);
+    vbin[v] = (uint16_t)bq;
+    atomicAdd(&counts[bq], 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // T <= 4096 sequential prefix: negligible next to the sweep
-    int run = 0;
-    for (int q = 0; q < T; ++q) {
-      cursor[q] = run;
-      run += counts[q];
-      endq[(int64_t)dl * T + q] = (uint16_t)run;
+  if (threadIdx.x == 0) {  // serial over bins: packet bases and per-packet metadata
+    int pk = 0, q = 0;
+    while (q < T && counts[q] == 0) ++q;
+    if (q > 0) meta[pk++] = q | (1 << 16);  // leading empty bins (q <= T <= 4096 < 65536)
+    while (q < T) {
+      int q2 = q + 1;
+      while (q2 < T && counts[q2] == 0) ++q2;
+      const int npk = (counts[q] + 3) / 4;
+      base[q] = pk;
+      for (int k = kMaxRun / 4 - 1; k < npk - 1; k += kMaxRun / 4) meta[pk + k] = 1 << 16;  // chunk split
+      meta[pk + npk - 1] = (q2 - q) | (1 << 16);
+      pk += npk;
+      q = q2;
     }
+    pk = (pk + 3) & ~3;  // whole groups of 4 packets (the tail packets are padding, no flags)
+    npk_total = pk;
+    prog_len[dl] = pk;
     int o = (sx > 0.f ? 1 : 0) | (sy > 0.f ? 2 : 0);
-    int pos = atomicAdd(&qcount[o], 1);
-    qlist[o * Dc + pos] = dl;
+    int slot = atomicAdd(&qcount[o], 1);
+    qlist[o * Dc + slot] = dl;
   }
   __syncthreads();
-  for (int v = threadIdx.x; v < HW; v += blockDim.x) {
-    int r = v / W, c = v % W;
-    double h = __dadd_rn(__dmul_rn((double)axis_coord(c, W, S), (double)sx), __dmul_rn((double)axis_coord(r, H, S), (double)sy));
-    int pos = atomicAdd(&cursor[alpha64(h, g)], 1);
-    perm[(int64_t)dl * HW + pos] = (uint16_t)v;
+  for (int v = threadIdx.x; v < HW; v += blockDim.x) {  // ids: any order within a bin
+    const int bq = vbin[v];
+    const int r = atomicAdd(&counts[bq], -1) - 1;
+    off[4 * base[bq] + r] = (uint32_t)v * 128u;
+  }
+  const int npk = npk_total;
+  for (int w = threadIdx.x; w < sweep_mask_words(HW, T); w += blockDim.x) {
+    uint32_t m = 0;
+    for (int j = 0; j < 32; ++j) {
+      const int k = w * 32 + j;
+      if (k < npk && (meta[k] >> 16)) m |= 1u << j;
+    }
+    mask[w] = m;
+  }
+  if (threadIdx.x == 0) {  // emit counts of the flagged packets, in order
+    int i = 0;
+    for (int k = 0; k < npk; ++k)
+      if (meta[k] >> 16) emitv[i++] = (uint16_t)(meta[k] & 0xFFFF);
   }
 }
 
@@ -145,17 +198,17 @@ constexpr int kSweepImgs = 64;   // images per CTA group: lane l owns images 2l,
 constexpr int kStageBins = 8;    // bins per staged output chunk
 constexpr int kStageStride = 68; // words per staged bin row (68 = 4 mod 32: conflict-free readout)
 constexpr int kBias = 255;       // cw in [-255, 255] -> biased u16 in [0, 510]
-constexpr int kMaxRun = 128;     // 128 * 510 < 65536: no carry between packed halves
 constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t sweep_pix_bytes(int HW) { return align16((size_t)HW * kPixStride); }
 // per-warp private area: its direction's sorted vertex ids and bin ends, and the output stage
 __host__ __device__ constexpr size_t sweep_warp_bytes(int HW, int T) {
-  return align16((size_t)HW * 2) + align16((size_t)T * 2) + (size_t)kStageBins * kStageStride * 4;
+  return (size_t)kStageBins * kStageStride * 4;  // output stage only: programs are read from L2
 }
+// cwb has HW + 1 rows: row HW is the padding row (bias = weight 0)
 __host__ __device__ constexpr size_t sweep_smem_bytes(int HW, int T) {
-  return (size_t)HW * 128 + sweep_pix_bytes(HW) + (size_t)kSweepWarps * sweep_warp_bytes(HW, T);
+  return align16((size_t)(HW + 1) * 128) + sweep_pix_bytes(HW) + (size_t)kSweepWarps * sweep_warp_bytes(HW, T);
 }
 
 template <typename OutT>
@@ -189,66 +242,88 @@ __device__ __forceinline__ void sweep_store_chunk(const int* __restrict__ st, Ou
   }
 }
 
-// One warp, one direction, the CTA's 64 images: walk the vertices in bin order and emit
-// the running (cumulative) sum at every bin end.  sid: this direction's vertex ids in
-// bin order (warp-private smem copy); send: send[q] = #{v : bin(v) <= q}.
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// One warp, one direction, the CTA's 64 images: run the direction's sweep program
+// (packets of 4 cw-row offsets), accumulating packed biased weights and emitting the
+// running (cumulative) sum for every bin.  prg: warp-private smem copy of the program;
+// lane4: shared-window address of this lane's column of the cw table.  Packets are
+// consumed four at a time: all 16 gathers are issued before the (warp-uniform)
+// end-of-chunk checks, so each warp keeps 16 shared loads in flight.
 template <typename OutT>
-__device__ __forceinline__ void sweep_direction(const uint32_t* __restrict__ cwb_lane, const uint16_t* __restrict__ sid,
-                                                const uint16_t* __restrict__ send, int* __restrict__ st,
-                                                OutT* __restrict__ out, int64_t img0, int nimg, int Dc, int dl, int T,
-                                                int lane) {
-  int i = 0, tot0 = 0, tot1 = 0;
-  for (int q0 = 0; q0 < T; q0 += kStageBins) {
-    const int qn = (T - q0) < kStageBins ? (T - q0) : kStageBins;
-    for (int qq = 0; qq < qn; ++qq) {
-      const int e = send[q0 + qq];
-      while (i < e) {  // warp-uniform run [i, e) of vertices in bin q0 + qq
-        const int cnt = (e - i) < kMaxRun ? (e - i) : kMaxRun;
-        const int stop = i + cnt;
-        uint32_t a = 0, b = 0;
-        int t = i;
-        switch (cnt & 3) {  // remainder first, then groups of 4 (independent loads)
-          case 3: a += cwb_lane[(uint32_t)sid[t++] * 32];  // fallthrough
-          case 2: b += cwb_lane[(uint32_t)sid[t++] * 32];  // fallthrough
-          case 1: a += cwb_lane[(uint32_t)sid[t++] * 32];  // fallthrough
-          default: break;
-        }
+__device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* __restrict__ prg, int npk,
+                                                int Lp, int nmask, int* __restrict__ st, OutT* __restrict__ out,
+                                                int64_t img0, int nimg, int Dc, int dl, int T, int lane) {
+  const uint4* pk = (const uint4*)prg;
+  const uint32_t* mask = prg + 4 * Lp;
+  const uint16_t* emitv = (const uint16_t*)(mask + nmask);
+  int q = 0, tot0 = 0, tot1 = 0, n = 0, ei = 0;
+  uint32_t a = 0;
+  uint32_t m = 0;
+  // software pipeline: the next group's 4 packets are loaded while this group gathers
+  uint4 w0 = __ldg(pk), w1 = __ldg(pk + 1), w2 = __ldg(pk + 2), w3 = __ldg(pk + 3);
 #pragma unroll 1
-        for (; t < stop; t += 4) {
-          const uint32_t v0 = sid[t], v1 = sid[t + 1], v2 = sid[t + 2], v3 = sid[t + 3];
-          a += cwb_lane[v0 * 32] + cwb_lane[v1 * 32];
-          b += cwb_lane[v2 * 32] + cwb_lane[v3 * 32];
-        }
-        a += b;
-        tot0 += (int)(a & 0xFFFFu) - kBias * cnt;
-        tot1 += (int)(a >> 16) - kBias * cnt;
-        i = stop;
-      }
-      *(int2*)(st + qq * kStageStride + 2 * lane) = make_int2(tot0, tot1);
+  for (int k = 0; k < npk; k += 4) {
+    if ((k & 31) == 0) m = __ldg(mask + (k >> 5));
+    uint32_t s[4];
+    s[0] = lds32(lane4 + w0.x) + lds32(lane4 + w0.y) + lds32(lane4 + w0.z) + lds32(lane4 + w0.w);
+    s[1] = lds32(lane4 + w1.x) + lds32(lane4 + w1.y) + lds32(lane4 + w1.z) + lds32(lane4 + w1.w);
+    s[2] = lds32(lane4 + w2.x) + lds32(lane4 + w2.y) + lds32(lane4 + w2.z) + lds32(lane4 + w2.w);
+    s[3] = lds32(lane4 + w3.x) + lds32(lane4 + w3.y) + lds32(lane4 + w3.z) + lds32(lane4 + w3.w);
+    if (k + 4 < npk) {
+      w0 = __ldg(pk + k + 4); w1 = __ldg(pk + k + 5); w2 = __ldg(pk + k + 6); w3 = __ldg(pk + k + 7);
     }
-    __syncwarp();
-    sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q0, lane);
-    __syncwarp();
+    if ((m & 0xFu) == 0) {  // no chunk end among these 4 packets
+      a += (s[0] + s[1]) + (s[2] + s[3]);
+      n += 4;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a += s[j];
+        ++n;
+        if (m & (1u << j)) {
+          tot0 += (int)(a & 0xFFFFu) - 4 * kBias * n;
+          tot1 += (int)(a >> 16) - 4 * kBias * n;
+          a = 0;
+          n = 0;
+          const int emit = __ldg(emitv + ei++);
+          for (int e = 0; e < emit; ++e) {
+            *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = make_int2(tot0, tot1);
+            ++q;
+            if ((q & (kStageBins - 1)) == 0 || q == T) {
+              __syncwarp();
+              sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, (q - 1) & ~(kStageBins - 1), lane);
+              __syncwarp();
+            }
+          }
+        }
+      }
+    }
+    m >>= 4;
   }
 }
 
 template <typename OutT>
 __global__ void __launch_bounds__(kSweepWarps * 32, 1)
-    k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint16_t* __restrict__ perm,
-              const uint16_t* __restrict__ endq, const int* __restrict__ qlist, const int* __restrict__ qcount,
+    k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint32_t* __restrict__ prog,
+              const int* __restrict__ prog_len, const int* __restrict__ qlist, const int* __restrict__ qcount,
               int Dc, int T, OutT* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int HW = H * W;
   uint32_t* cwb = (uint32_t*)smem;                 // [HW][32] words: images (2l, 2l+1) biased u16
-  uint8_t* pix = smem + (size_t)HW * 128;          // [HW][kPixStride] u8 (64 used)
+  uint8_t* pix = smem + align16((size_t)(HW + 1) * 128);  // [HW][kPixStride] u8 (64 used)
   unsigned char* wbase = pix + sweep_pix_bytes(HW) + (size_t)(threadIdx.x >> 5) * sweep_warp_bytes(HW, T);
-  uint16_t* sid = (uint16_t*)wbase;                               // [HW]
-  uint16_t* send = (uint16_t*)(wbase + align16((size_t)HW * 2));  // [T]
-  int* st = (int*)(wbase + align16((size_t)HW * 2) + align16((size_t)T * 2));  // [kStageBins][kStageStride]
+  const int Lp = sweep_prog_packets(HW, T), Lw = sweep_prog_words(HW, T), nmask = sweep_mask_words(HW, T);
+  int* st = (int*)wbase;                                             // [kStageBins][kStageStride]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* cwb_lane = cwb + lane;
+  const uint32_t lane4 = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
   const int qc0 = qcount[0], qc1 = qcount[1], qc2 = qcount[2], qc3 = qcount[3];
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
+  if (threadIdx.x < 32) cwb[HW * 32 + threadIdx.x] = (uint32_t)kBias | ((uint32_t)kBias << 16);  // padding row
 
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t img0 = grp * kSweepImgs;
@@ -256,9 +331,11 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
     __syncthreads();  // the previous group's sweeps are done with pix / cwb
     // stage the group's pixels transposed: pix[v][i] (16-byte global loads when aligned)
     if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
+      // thread -> (image i = t % 64, 16-pixel block); a warp stores 32 images' bytes of one
+      // pixel into one staged row: conflict-free byte stores
       const int per = HW >> 4;
       for (int f = threadIdx.x; f < kSweepImgs * per; f += blockDim.x) {
-        const int i = f / per, v = (f - i * per) << 4;
+        const int i = f & (kSweepImgs - 1), v = (f >> 6) << 4;
         uint4 x = make_uint4(0, 0, 0, 0);
         if (i < nimg) x = __ldcs((const uint4*)(img + (img0 + i) * HW + v));
         const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
@@ -267,8 +344,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       }
     } else {
       for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
-        const int i = f / HW, v = f - i * HW;
-        pix[v * kPixStride + i] = i < nimg ? __ldcs(img + (img0 + i) * HW + v) : (uint8_t)0;
+        const int i = f & (kSweepImgs - 1), v = f >> 6;
+        pix[v * kPixStride + i] = i < nimg ? img[(img0 + i) * HW + v] : (uint8_t)0;
       }
     }
 #pragma unroll 1
@@ -278,26 +355,21 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       __syncthreads();  // pix staged / previous quadrant's sweeps done with cwb
       const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
       {
-        // element (v, l): v advances by 16 per iteration (512 threads / 32 lanes)
-        const int l = lane;
+        // element (v, lane): cw of images 2l, 2l+1 in packed u16x2 arithmetic.
+        // packed = (a + 255 + m_diag) - (m_c + m_r) stays >= 0 per half (cw >= -255).
         int v = threadIdx.x >> 5;
         int r = v / W, c = v - r * W;
-        const int step_r = 16 / W, step_c = 16 - step_r * W;
-        for (; v < HW; v += 16) {
+        const int step_r = kSweepWarps / W, step_c = kSweepWarps - step_r * W;
+        for (; v < HW; v += kSweepWarps) {
           const bool vc = (unsigned)(c + dc) < (unsigned)W, vr = (unsigned)(r + dr) < (unsigned)H;
-          const uint8_t* p0 = pix + v * kPixStride + 2 * l;
-          const uint32_t a2 = *(const uint16_t*)p0;
-          uint32_t packed = 0;
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int a = (a2 >> (8 * k)) & 0xFF;
-            int cw = a, mc = 0, mr = 0;
-            if (vc) { mc = max(a, (int)p0[dc * kPixStride + k]); cw -= mc; }
-            if (vr) { mr = max(a, (int)p0[dr * W * kPixStride + k]); cw -= mr; }
-            if (vc && vr) cw += max(max(mc, mr), (int)p0[(dr * W + dc) * kPixStride + k]);
-            packed |= (uint32_t)(cw + kBias) << (16 * k);
-          }
-          cwb[v * 32 + l] = packed;
+          const uint8_t* p0 = pix + v * kPixStride + 2 * lane;
+          const uint32_t A = __byte_perm(*(const uint16_t*)p0, 0, 0x4140);
+          uint32_t MC = 0, MR = 0, MD = 0;
+          if (vc) MC = __vmaxu2(A, __byte_perm(*(const uint16_t*)(p0 + dc * kPixStride), 0, 0x4140));
+          if (vr) MR = __vmaxu2(A, __byte_perm(*(const uint16_t*)(p0 + dr * W * kPixStride), 0, 0x4140));
+          if (vc && vr)
+            MD = __vmaxu2(__vmaxu2(MC, MR), __byte_perm(*(const uint16_t*)(p0 + (dr * W + dc) * kPixStride), 0, 0x4140));
+          cwb[v * 32 + lane] = (A + 0x00FF00FFu + MD) - (MC + MR);
           r += step_r;
           c += step_c;
           if (c >= W) { c -= W; ++r; }
@@ -306,13 +378,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       __syncthreads();
       for (int k = warp; k < qco; k += kSweepWarps) {
         const int dl = qlist[o * Dc + k];
-        // warp-private copies of this direction's tables
-        const uint16_t* P = perm + (int64_t)dl * HW;
-        const uint16_t* E = endq + (int64_t)dl * T;
-        for (int t = lane; t < HW; t += 32) sid[t] = P[t];
-        for (int t = lane; t < T; t += 32) send[t] = E[t];
-        __syncwarp();
-        sweep_direction<OutT>(cwb_lane, sid, send, st, out, img0, nimg, Dc, dl, T, lane);
+        sweep_direction<OutT>(lane4, prog + (int64_t)dl * Lw, prog_len[dl], Lp, nmask, st, out, img0, nimg, Dc, dl,
+                              T, lane);
         __syncwarp();
       }
     }
@@ -457,19 +524,23 @@ wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs,
 bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
   if (ndim != 2) return false;
   int64_t HW = dims[0] * dims[1];
-  return HW >= 1 && HW <= 1024 && T <= 65535 && sweep_smem_bytes((int)HW, T) <= 227 * 1024;
+  return HW >= 1 && HW <= 1023 && T <= 4096 && sweep_smem_bytes((int)HW, T) <= 227 * 1024;
 }
 
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc,
                            int T, const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                            int num_sms) {
   const int HW = H * W;
-  uint16_t* perm = (uint16_t*)scratch;
-  uint16_t* endq = perm + (size_t)Dc * HW;
-  int* qcount = (int*)(((uintptr_t)(endq + (size_t)Dc * T) + 15) & ~(uintptr_t)15);
-  int* qlist = qcount + 4;
+  const int Lp = sweep_prog_packets(HW, T);
+  uint32_t* prog = (uint32_t*)scratch;
+  int* ints = (int*)(((uintptr_t)(prog + (size_t)Dc * sweep_prog_words(HW, T)) + 15) & ~(uintptr_t)15);
+  int* qcount = ints;
+  int* prog_len = ints + 4;
+  int* qlist = prog_len + Dc;
   WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 4 * sizeof(int), st));
-  k_sort2d<<<Dc, 256, 2 * T * sizeof(int), st>>>(H, W, dirs, d_begin, Dc, gp, perm, endq, qlist, qcount); count_launch();
+  const size_t sort_smem = (size_t)(2 * T + Lp) * sizeof(int) + align16((size_t)HW * 2);
+  if (sort_smem > 48 * 1024) WECT_CUDA_TRY(cudaFuncSetAttribute(k_sort2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
+  k_sort2d<<<Dc, 256, sort_smem, st>>>(H, W, dirs, d_begin, Dc, gp, prog, prog_len, qlist, qcount); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   const size_t smem = sweep_smem_bytes(HW, T);
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
@@ -477,11 +548,11 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   MainTimer timer(st);
   if (odtype == WECT_I32) {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_sweep2d<int32_t><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, perm, endq, qlist, qcount, Dc, T,
+    k_sweep2d<int32_t><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, prog, prog_len, qlist, qcount, Dc, T,
                                                              (int32_t*)out); count_launch();
   } else {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_sweep2d<long long><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, perm, endq, qlist, qcount, Dc, T,
+    k_sweep2d<long long><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, prog, prog_len, qlist, qcount, Dc, T,
                                                                (long long*)out); count_launch();
   }
   timer.stop();
@@ -490,7 +561,7 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
 }
 
 size_t sweep2d_scratch_bytes(int HW, int Dc, int T) {
-  return (size_t)Dc * HW * 2 + (size_t)Dc * T * 2 + 16 + 16 + (size_t)4 * Dc * 4 + 64;
+  return (size_t)Dc * sweep_prog_words(HW, T) * 4 + 16 + (size_t)(4 + Dc + 4 * Dc) * 4 + 64;
 }
 
 // histogram path over a chunk of images [b0, b0 + nb): cwo scratch for nb images, diff rows at b0
