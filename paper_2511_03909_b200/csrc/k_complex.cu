@@ -110,7 +110,7 @@ __global__ void k_absmax_i32(const int32_t* __restrict__ w, int64_t n, unsigned 
 }
 
 // mode 0: WECT (M64 bits + R from pass 1), mode 1: ECF (M32 bits)
-__global__ void k_complex_params(int mode, int n, const unsigned long long* __restrict__ m64_bits,
+__global__ void k_params_complex(int mode, int n, const unsigned long long* __restrict__ m64_bits,
                                  const unsigned int* __restrict__ m32_bits, const unsigned int* __restrict__ r1_bits,
                                  const unsigned int* __restrict__ smax_bits, int T, double maxheight, double lo_in, double hi_in, uint32_t flags,
                                  GridParams* __restrict__ out) {
@@ -139,111 +139,256 @@ __global__ void k_check_indices(const int32_t* __restrict__ v, int64_t n, int64_
     if ((uint32_t)v[i] >= (uint64_t)k0 || v[i] < 0) { atomicOr(flag, 1u); return; }
 }
 
-// --------------------------------------------------------------- main kernel
-// grid = (filter tiles of 32, cell slices); lanes = filters, warps = cell streams.
-// MODE 0 (WECT): h(v, p) = <coords[v], dirs[p]> (fp32 FMA fast path, binary64 repair).
-// MODE 1 (ECF):  h(v, p) = fvals[v * m + p].
-template <int MODE, int N, bool FLOATW>
+// --------------------------------------------------------------- main kernels
+// Flush of a lane-interleaved histogram hist[q * 32 + lane] (lanes = 32 filter rows):
+// every lane's atomics hit its own bank, whatever the bins.
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ void flush_hist_t(Acc* hist, int T, int row0, int Dc, void* diff) {
+  for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) {
+    const int q = i >> 5, r = i & 31;
+    const Acc val = hist[i];
+    if (val != (Acc)0 && row0 + r < Dc) {
+      const int64_t o = (int64_t)(row0 + r) * T + q;
+      if (FLOATW) atomicAdd((double*)diff + o, (double)val);
+      else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
+    }
+    hist[i] = (Acc)0;
+  }
+}
+
+// Histogram flush into the global difference table (int64 / binary64); zeroes the rows.
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ void flush_hist(Acc* hist, int rows, int T, int TS, int row0, int Dc, void* diff) {
+  for (int i = threadIdx.x; i < rows * T; i += blockDim.x) {
+    const int r = i / T, q = i - r * T;
+    const Acc val = hist[r * TS + q];
+    if (val != (Acc)0 && row0 + r < Dc) {
+      const int64_t o = (int64_t)(row0 + r) * T + q;
+      if (FLOATW) atomicAdd((double*)diff + o, (double)val);
+      else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
+    }
+    hist[r * TS + q] = (Acc)0;
+  }
+}
+
+// Signed weight (-1)^dim w of cell b of segment S, accumulator type.
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ Acc cell_weight(const Seg& S, int64_t b) {
+  Acc w;
+  if (FLOATW) w = S.weights ? __ldg((const float*)S.weights + b) : 1.f;
+  else w = S.weights ? __ldg((const int*)S.weights + b) : 1;
+  return S.sign < 0 ? -w : w;
+}
+
+__device__ __forceinline__ int64_t chunk_cells(bool floatw, int64_t float_chunk, const unsigned int* wmax_bits,
+                                               int64_t span) {
+  // int32 partials: chunk * max|w| < 2^31; float partials are flushed every float_chunk cells
+  if (floatw) return float_chunk;
+  const unsigned int wm = *wmax_bits;
+  int64_t chunk = wm == 0 ? span : (int64_t)(2147483647u / wm);
+  return chunk < 1 ? 1 : chunk;
+}
+
+// WECT of an explicit complex.  grid = (direction tiles of 32, cell slices); lanes =
+// directions, warps = contiguous cell streams.  Cells are taken in batches: the warp
+// first gathers a batch's vertex coordinates lane-parallel into a private smem buffer
+// (many independent loads in flight), then each lane evaluates the batch against its own
+// direction from broadcast reads: h = <x, s> by fp32 FMA (binary64 repair near bin
+// edges, reading A1), cell height = max over its vertices (rmax, eq. msi),
+// one shared-memory atomic per (cell, direction) (scatter_add).
+constexpr int kBatchFloats = 1536;  // per-warp coordinate buffer (6 KB)
+
+// binary64 repair of one cell's bin: exact heights of its vertices (axis order), max,
+// alpha64 (reading A1).  Out of line: it runs for ~0.1% of (cell, direction) pairs.
+template <int N, int NP>
+__device__ __noinline__ int cell_repair(const float* xs, int ar, const float* s, const GridParams* gp) {
+  double hm = -DBL_MAX;
+  for (int t = 0; t < ar; ++t) {
+    double h = __dmul_rn((double)xs[t * NP], (double)s[0]);
+    for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)xs[t * NP + i], (double)s[i]));
+    hm = fmax(hm, h);
+  }
+  note_repair();
+  return alpha64(hm, *gp);
+}
+
+__device__ __forceinline__ void red_shared(uint32_t addr, int w) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(w));
+}
+__device__ __forceinline__ void red_shared(uint32_t addr, float w) { atomicAdd((float*)__cvta_shared_to_generic(addr), w); }
+
+// One batch of nb cells of arity AR (0: runtime arity `arr`) against this lane's direction.
+template <int N, int NP, int AR, bool FLOATW, typename Acc>
+__device__ __forceinline__ void batch_eval(const float* xb, int nb, unsigned badcells, Acc wl, const float* s,
+                                           const GridParams& g, const GridParams* gp, uint32_t hlane, bool active,
+                                           int arr = AR) {
+  const int ar = AR > 0 ? AR : arr;
+  const float A = g.A, Bc = g.B, tau = g.fp32_only ? -1.f : g.tau;
+  const int Tm1 = g.T - 1;
+  for (int j = 0; j < nb; ++j) {
+    const Acc w = __shfl_sync(0xffffffffu, wl, j);
+    if ((badcells >> j) & 1u) continue;  // a cell with an out-of-range index is skipped
+    const float4* xc = (const float4*)(xb + j * ar * NP);
+    float hmax = -FLT_MAX;
+#pragma unroll
+    for (int t = 0; t < (AR > 0 ? AR : 1); ++t) {
+      for (int tt = t; tt < (AR > 0 ? t + 1 : ar); ++tt) {
+        float x[NP];
+#pragma unroll
+        for (int i4 = 0; i4 < NP / 4; ++i4) {
+          const float4 q4 = xc[tt * (NP / 4) + i4];  // broadcast LDS.128
+          x[4 * i4] = q4.x; x[4 * i4 + 1] = q4.y; x[4 * i4 + 2] = q4.z; x[4 * i4 + 3] = q4.w;
+        }
+        float h = x[0] * s[0];
+#pragma unroll
+        for (int i = 1; i < N; ++i) h = fmaf(x[i], s[i], h);
+        hmax = fmaxf(hmax, h);
+      }
+    }
+    const float u = fmaf(hmax, A, Bc);
+    int bin = __float2int_ru(u);
+    if (fabsf(u - rintf(u)) < tau) bin = cell_repair<N, NP>((const float*)xc, ar, s, gp);
+    else bin = bin < 0 ? 0 : (bin > Tm1 ? Tm1 : bin);
+    if (active && w != (Acc)0) red_shared(hlane + 128u * (uint32_t)bin, w);
+  }
+}
+
+template <int N, bool FLOATW>
 __global__ void __launch_bounds__(256) k_complex(Segs segs, const float* __restrict__ coords, int64_t k0,
-                                                 const float* __restrict__ fsrc, int m_or_D, int d_begin, int Dc,
+                                                 const float* __restrict__ dirs, int d_begin, int Dc,
                                                  const GridParams* __restrict__ gp,
                                                  const unsigned int* __restrict__ wmax_bits, int64_t slice_len,
                                                  int64_t float_chunk, void* __restrict__ diff) {
   using Acc = typename std::conditional<FLOATW, float, int>::type;
   extern __shared__ __align__(16) unsigned char smraw[];
-  Acc* hist = (Acc*)smraw;  // [32][T+1]
+  const GridParams g = *gp;
+  const int T = g.T;
+  Acc* hist = (Acc*)smraw;  // [T][32] lane-interleaved
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  constexpr int NP = (N + 3) & ~3;  // vertex coordinates padded to whole float4s
+  float* xb = (float*)(smraw + (size_t)32 * T * sizeof(Acc)) + warp * kBatchFloats;
   __shared__ Seg ssegs[kMaxSegs];
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < kMaxSegs; ++i) ssegs[i] = segs.s[i];  // constant indices: no local copy
   }
-  const GridParams g = *gp;
-  const int T = g.T, TS = T + 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) hist[i] = (Acc)0;
   const int dl = blockIdx.x * 32 + lane;
   const bool active = dl < Dc;
   const int p = d_begin + (active ? dl : 0);
-  float s[N > 0 ? N : 1];
-  if (MODE == 0) {
+  const uint32_t hlane = (uint32_t)__cvta_generic_to_shared(hist) + 4u * lane;
+  float s[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) s[i] = fsrc[p * N + i];
-  }
+  for (int i = 0; i < N; ++i) s[i] = dirs[p * N + i];
   const int64_t c0 = blockIdx.y * slice_len;
   const int64_t c1 = (c0 + slice_len) < segs.total ? (c0 + slice_len) : segs.total;
-  // chunking: int32 partials must not overflow (chunk * max|w| < 2^31); float partials are
-  // flushed every float_chunk cells (reading A8 error bound)
-  int64_t chunk;
-  if (FLOATW) chunk = float_chunk;
-  else {
-    unsigned int wm = *wmax_bits;
-    chunk = wm == 0 ? c1 - c0 : (int64_t)(2147483647u / wm);
-    if (chunk < 1) chunk = 1;
-  }
-  int seg = 0;
+  const int64_t chunk = chunk_cells(FLOATW, float_chunk, wmax_bits, c1 - c0);
+  __syncthreads();
   for (int64_t a0 = c0; a0 < c1; a0 += chunk) {
     const int64_t a1 = (a0 + chunk) < c1 ? (a0 + chunk) : c1;
-    for (int i = threadIdx.x; i < 32 * TS; i += blockDim.x) hist[i] = (Acc)0;
+    const int64_t per = (a1 - a0 + nwarps - 1) / nwarps;
+    const int64_t w0 = a0 + warp * per, w1 = (w0 + per) < a1 ? (w0 + per) : a1;
+    int seg = 0;
+    for (int64_t c = w0; c < w1;) {
+      while (c >= ssegs[seg].start + ssegs[seg].count) ++seg;
+      const Seg& S = ssegs[seg];
+      const int ar = S.arity;
+      int nb = kBatchFloats / (ar * NP);
+      nb = nb > 32 ? 32 : nb;
+      const int64_t lim = S.start + S.count < w1 ? S.start + S.count : w1;
+      if (c + nb > lim) nb = (int)(lim - c);
+      const int64_t b0 = c - S.start;
+      // phase A: lane-parallel gathers of the batch's vertex coordinates
+      unsigned badcells = 0;  // bit j: cell j has an out-of-range index
+      for (int t = lane; t < nb * ar; t += 32) {
+        int v = S.verts ? __ldg(S.verts + b0 * ar + t) : (int)(b0 + t);
+        if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
+        const float* x = coords + (int64_t)v * N;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) xb[t * NP + i] = i < N ? __ldg(x + i) : 0.f;
+      }
+      Acc wl = (Acc)0;
+      if (lane < nb) wl = cell_weight<FLOATW, Acc>(S, b0 + lane);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) badcells |= __shfl_xor_sync(0xffffffffu, badcells, o);
+      if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
+      __syncwarp();
+      // phase B: lanes = directions (arity specialised so the vertex loops unroll)
+      switch (ar) {
+        case 1: batch_eval<N, NP, 1, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active); break;
+        case 2: batch_eval<N, NP, 2, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active); break;
+        case 3: batch_eval<N, NP, 3, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active); break;
+        case 4: batch_eval<N, NP, 4, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active); break;
+        case 5: batch_eval<N, NP, 5, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active); break;
+        case 8: batch_eval<N, NP, 8, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active); break;
+        default: batch_eval<N, NP, 0, FLOATW>(xb, nb, badcells, wl, s, g, gp, hlane, active, ar); break;
+      }
+      __syncwarp();
+      c += nb;
+    }
     __syncthreads();
-    for (int64_t c = a0 + warp; c < a1; c += nwarps) {
+    flush_hist_t<FLOATW, Acc>(hist, T, blockIdx.x * 32, Dc, diff);
+    __syncthreads();
+  }
+}
+
+// ECF (Alg. 1 with given filters, few of them): thread per cell, a tile of up to
+// kEcfTile filters per CTA (grid.x); FVals gathered from fvals[v * m + p].
+constexpr int kEcfTile = 8;
+
+template <bool FLOATW>
+__global__ void __launch_bounds__(256) k_ecf(Segs segs, int64_t k0, const float* __restrict__ fvals, int m,
+                                             int d_begin, int Dc, const GridParams* __restrict__ gp,
+                                             const unsigned int* __restrict__ wmax_bits, int64_t slice_len,
+                                             int64_t float_chunk, void* __restrict__ diff) {
+  using Acc = typename std::conditional<FLOATW, float, int>::type;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const GridParams g = *gp;
+  const int T = g.T, TS = T + 1;
+  Acc* hist = (Acc*)smraw;  // [kEcfTile][T+1]
+  __shared__ Seg ssegs[kMaxSegs];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < kMaxSegs; ++i) ssegs[i] = segs.s[i];
+  }
+  const int p0 = d_begin + blockIdx.x * kEcfTile;
+  const int np = (Dc - (int)blockIdx.x * kEcfTile) < kEcfTile ? (Dc - (int)blockIdx.x * kEcfTile) : kEcfTile;
+  for (int i = threadIdx.x; i < kEcfTile * TS; i += blockDim.x) hist[i] = (Acc)0;
+  const int64_t c0 = blockIdx.y * slice_len;
+  const int64_t c1 = (c0 + slice_len) < segs.total ? (c0 + slice_len) : segs.total;
+  const int64_t chunk = chunk_cells(FLOATW, float_chunk, wmax_bits, c1 - c0);
+  __syncthreads();
+  for (int64_t a0 = c0; a0 < c1; a0 += chunk) {
+    const int64_t a1 = (a0 + chunk) < c1 ? (a0 + chunk) : c1;
+    int seg = 0;
+    for (int64_t c = a0 + threadIdx.x; c < a1; c += blockDim.x) {
       while (c >= ssegs[seg].start + ssegs[seg].count) ++seg;
       const Seg& S = ssegs[seg];
       const int64_t b = c - S.start;
       const int ar = S.arity;
-      float hmax = -FLT_MAX;
-      bool bad = false;
-      for (int j = 0; j < ar; ++j) {
-        int v = S.verts ? __ldg(S.verts + b * ar + j) : (int)b;
-        if ((uint64_t)(int64_t)v >= (uint64_t)k0) { bad = true; v = 0; }
-        float h;
-        if (MODE == 0) {
-          const float* x = coords + (int64_t)v * N;
-          h = __ldg(x) * s[0];
-#pragma unroll
-          for (int i = 1; i < N; ++i) h = fmaf(__ldg(x + i), s[i], h);
-        } else {
-          h = __ldg(fsrc + (int64_t)v * m_or_D + p);
+      const Acc w = cell_weight<FLOATW, Acc>(S, b);
+      for (int pp = 0; pp < np; ++pp) {
+        float hmax = -FLT_MAX;
+        bool bad = false;
+        for (int t = 0; t < ar; ++t) {
+          int v = S.verts ? __ldg(S.verts + b * ar + t) : (int)b;
+          if ((uint64_t)(int64_t)v >= (uint64_t)k0) { bad = true; v = 0; }
+          hmax = fmaxf(hmax, __ldg(fvals + (int64_t)v * m + p0 + pp));
         }
-        hmax = fmaxf(hmax, h);
-      }
-      if (bad) {
-        if (lane == 0) atomicOr(&g_err_word, 1u);
-        continue;
-      }
-      int bin = alpha32_or_repair(hmax, g);
-      if (bin < 0) {
-        double hm = -DBL_MAX;
-        for (int j = 0; j < ar; ++j) {
-          const int v = S.verts ? __ldg(S.verts + b * ar + j) : (int)b;
-          double h;
-          if (MODE == 0) {
-            const float* x = coords + (int64_t)v * N;
-            h = __dmul_rn((double)x[0], (double)s[0]);
-#pragma unroll
-            for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x[i], (double)s[i]));
-          } else {
-            h = (double)fsrc[(int64_t)v * m_or_D + p];
-          }
-          hm = fmax(hm, h);
+        if (bad) {
+          atomicOr(&g_err_word, 1u);
+          break;
         }
-        bin = alpha64(hm, g);
-        note_repair();
+        int bin = alpha32_or_repair(hmax, g);
+        if (bin < 0) {
+          bin = alpha64((double)hmax, g);  // filter values are exact in binary64
+          note_repair();
+        }
+        if (w != (Acc)0) atomicAdd(&hist[pp * TS + bin], w);
       }
-      Acc w;
-      if (FLOATW) w = S.weights ? __ldg((const float*)S.weights + b) : 1.f;
-      else w = S.weights ? __ldg((const int*)S.weights + b) : 1;
-      if (S.sign < 0) w = -w;
-      if (active && w != (Acc)0) atomicAdd(&hist[lane * TS + bin], w);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) {
-      const int r = i / T, q = i - r * T;
-      const Acc val = hist[r * TS + q];
-      if (val != (Acc)0 && blockIdx.x * 32 + r < Dc) {
-        const int64_t o = (int64_t)(blockIdx.x * 32 + r) * T + q;
-        if (FLOATW) atomicAdd((double*)diff + o, (double)val);
-        else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
-      }
-    }
+    flush_hist<FLOATW, Acc>(hist, np, T, TS, blockIdx.x * kEcfTile, Dc, diff);
     __syncthreads();
   }
 }
@@ -272,35 +417,58 @@ __global__ void k_finalize(const In* __restrict__ diff, int64_t rows, int T, Out
 }
 
 // ------------------------------------------------------------------ launchers
-template <int MODE, int N>
-static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* coords, int64_t k0, const float* fsrc,
-                                    int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
-                                    const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
-  const int tiles = (Dc + 31) / 32;
-  const size_t smem = (size_t)32 * (T + 1) * 4;
-  // slices: >= 2 waves of CTAs, each slice <= 2^20 cells
-  int64_t total = segs.total;
-  int per_sm = (int)((220 * 1024) / (smem + 2048));
-  if (per_sm < 1) per_sm = 1;
-  if (per_sm > 8) per_sm = 8;
+static int64_t pick_slice(int64_t total, int tiles, int per_sm, int num_sms, int64_t cap) {
   int64_t want = ((int64_t)num_sms * per_sm * 2 + tiles - 1) / tiles;
   int64_t slice = (total + want - 1) / want;
-  if (slice > ((int64_t)1 << 20)) slice = (int64_t)1 << 20;
+  if (slice > cap) slice = cap;
   if (slice < 256) slice = 256;
-  int64_t nslices = (total + slice - 1) / slice;
-  if (nslices < 1) nslices = 1;
-  dim3 grid(tiles, (unsigned)nslices);
-  const int64_t fchunk = 4096;
+  return slice;
+}
+
+template <int N>
+static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* coords, int64_t k0, const float* dirs,
+                                    int d_begin, int Dc, int T, const GridParams* gp, const unsigned int* wmax,
+                                    void* diff, cudaStream_t st, int num_sms) {
+  const int tiles = (Dc + 31) / 32;
+  const size_t smem = (size_t)32 * T * 4 + (size_t)8 * kBatchFloats * 4;
+  int per_sm = (int)((220 * 1024) / (smem + 2048));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  const int64_t slice = pick_slice(segs.total, tiles, per_sm, num_sms, (int64_t)1 << 20);
+  dim3 grid(tiles, (unsigned)((segs.total + slice - 1) / slice));
   MainTimer timer(st);
   if (floatw) {
-    auto k = k_complex<MODE, N, true>;
+    auto k = k_complex<N, true>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff); count_launch();
+    k<<<grid, 256, smem, st>>>(segs, coords, k0, dirs, d_begin, Dc, gp, wmax, slice, 4096, diff);
   } else {
-    auto k = k_complex<MODE, N, false>;
+    auto k = k_complex<N, false>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, st>>>(segs, coords, k0, fsrc, m_or_D, d_begin, Dc, gp, wmax, slice, fchunk, diff); count_launch();
+    k<<<grid, 256, smem, st>>>(segs, coords, k0, dirs, d_begin, Dc, gp, wmax, slice, 4096, diff);
   }
+  count_launch();
+  timer.stop();
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+static wect_status launch_ecf(bool floatw, const Segs& segs, int64_t k0, const float* fvals, int m, int d_begin, int Dc,
+                              int T, const GridParams* gp, const unsigned int* wmax, void* diff, cudaStream_t st,
+                              int num_sms) {
+  const int tiles = (Dc + kEcfTile - 1) / kEcfTile;
+  const size_t smem = (size_t)kEcfTile * (T + 1) * 4;
+  int per_sm = (int)((220 * 1024) / (smem + 2048));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  const int64_t slice = pick_slice(segs.total, tiles, per_sm, num_sms, (int64_t)1 << 20);
+  dim3 grid(tiles, (unsigned)((segs.total + slice - 1) / slice));
+  MainTimer timer(st);
+  if (floatw) {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ecf<true><<<grid, 256, smem, st>>>(segs, k0, fvals, m, d_begin, Dc, gp, wmax, slice, 4096, diff);
+  } else {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ecf<false><<<grid, 256, smem, st>>>(segs, k0, fvals, m, d_begin, Dc, gp, wmax, slice, 4096, diff);
+  }
+  count_launch();
   timer.stop();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
@@ -309,10 +477,10 @@ static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* 
 wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                            const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
                            const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
-  if (mode == 1) return launch_complex_n<1, 0>(floatw, segs, coords, k0, fsrc, m_or_D, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
+  if (mode == 1) return launch_ecf(floatw, segs, k0, fsrc, m_or_D, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
   switch (n) {
 #define WECT_CASE(NN) \
-  case NN: return launch_complex_n<0, NN>(floatw, segs, coords, k0, fsrc, m_or_D, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
+  case NN: return launch_complex_n<NN>(floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
     WECT_CASE(1) WECT_CASE(2) WECT_CASE(3) WECT_CASE(4) WECT_CASE(5) WECT_CASE(6) WECT_CASE(7) WECT_CASE(8)
 #undef WECT_CASE
   }
@@ -350,7 +518,7 @@ wect_status launch_vmax(int n, const float* coords, int64_t k0, const float* dir
 wect_status launch_complex_params(int mode, int n, const unsigned long long* m64, const unsigned int* m32,
                                   const unsigned int* r1, const unsigned int* smax, const wect_grid& grid,
                                   GridParams* gp, cudaStream_t st) {
-  k_complex_params<<<1, 1, 0, st>>>(mode, n, m64, m32, r1, smax, grid.T, grid.maxheight, grid.lo, grid.hi,
+  k_params_complex<<<1, 1, 0, st>>>(mode, n, m64, m32, r1, smax, grid.T, grid.maxheight, grid.lo, grid.hi,
                                     grid.flags, gp); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;

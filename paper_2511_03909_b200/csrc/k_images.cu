@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Histogram path: orthant-combined weights cwo[b][v][o] (int16), o = sum_k (s_k > 0) << k.
+// Histogram path: orthant-combined weights cwo[b][o][v] (int16, octant-major), o = sum_k (s_k > 0) << k.
 // cw_o(v) = sum over axis subsets A (cells anchored at v, extending one step along each
 // k in A toward -1 if bit k of o is set, else +1) of (-1)^|A| * max over the cell corners.
 // ---------------------------------------------------------------------------
@@ -439,21 +439,41 @@ __global__ void __launch_bounds__(256) k_grid_cw(const uint8_t* __restrict__ img
       res[o] = (int16_t)cw;
     }
 #pragma unroll
-    for (int o = 0; o < NO; ++o) cwo[f * NO + o] = res[o];
+    for (int o = 0; o < NO; ++o) cwo[(b * NO + o) * nv + v] = res[o];  // octant-major rows
   }
+}
+
+// lanes = 32 directions, each warp streams whole grid rows (x fastest).  Per row the
+// lane folds everything but the x term into one constant, so a voxel costs one FMA:
+//     u = fmaf((float)x, A s0 / S, U0),  U0 = A (y s1 + z s2 - s0 (L0-1)/(2S)) + B,
+// an approximation of (T-1)(h - lo)/(hi - lo) within the guard tau (A1:
+// tau = 2 eps (A (n+2) R + 2|B| + T + 1) bounds this evaluation's error too); voxels whose
+// u lies within tau of an integer recompute h exactly in binary64 from the axis tables.
+// The row's orthant weights are staged in smem with coalesced 16-byte loads; the
+// histogram is lane-interleaved [T][32] so atomics never bank-conflict.
+constexpr int kSegVox = 256;     // voxels per staged row segment
+constexpr int kSegStride = 264;  // int16 per staged octant row (132 words = 4 mod 32: conflict-free)
+
+__device__ __noinline__ int grid_repair(int x, float cx, float cy, float cz, const float* s, int nd,
+                                        const GridParams* gp) {
+  double h64 = __dadd_rn(__dmul_rn((double)cx, (double)s[0]), __dmul_rn((double)cy, (double)s[1]));
+  if (nd == 3) h64 = __dadd_rn(h64, __dmul_rn((double)cz, (double)s[2]));
+  note_repair();
+  return alpha64(h64, *gp);
 }
 
 template <int ND>
 __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ cwo, int64_t d0, int64_t d1, int64_t d2,
                                                    const float* __restrict__ dirs, int d_begin, int Dc,
-                                                   const GridParams* __restrict__ gp, int64_t slice_len,
+                                                   const GridParams* __restrict__ gp, int64_t slice_rows,
                                                    int64_t b_offset, unsigned long long* __restrict__ diff) {
   constexpr int NO = 1 << ND;
-  extern __shared__ int hist[];  // [32][T+1]
+  extern __shared__ __align__(16) int hist[];  // [T][32] lane-interleaved, then per-warp cw segments
   __shared__ float axc[3][1024];
   const GridParams g = *gp;
-  const int T = g.T, TS = T + 1;
+  const int T = g.T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int16_t* seg = (int16_t*)(hist + 32 * T) + warp * NO * kSegStride;  // [NO][kSegStride]
   int L[3];
   if (ND == 2) { L[0] = (int)d1; L[1] = (int)d0; L[2] = 1; } else { L[0] = (int)d2; L[1] = (int)d1; L[2] = (int)d0; }
   int maxd = L[0] > L[1] ? L[0] : L[1];
@@ -461,7 +481,7 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
   const double S = (double)(maxd - 1 > 1 ? maxd - 1 : 1);
   for (int k = 0; k < ND; ++k)
     for (int i = threadIdx.x; i < L[k]; i += blockDim.x) axc[k][i] = axis_coord(i, L[k], S);
-  for (int i = threadIdx.x; i < 32 * TS; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) hist[i] = 0;
   const int dl = blockIdx.x * 32 + lane;
   const bool active = dl < Dc;
   const int p = d_begin + (active ? dl : 0);
@@ -472,39 +492,65 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
     s[k] = dirs[p * ND + k];
     o |= (s[k] > 0.f ? 1 : 0) << k;
   }
-  const int64_t nv = (int64_t)L[0] * L[1] * L[2];
+  const float A = g.A, Bc = g.B, tau = g.fp32_only ? -1.f : g.tau;
+  const float a0 = A * s[0] / (float)S;
+  const float c0 = (float)((double)(L[0] - 1) / 2.0);
+  const bool clampit = g.lo != -g.M || g.hi != g.M || g.degenerate;
+  const int Tm1 = T - 1;
+  const uint32_t hlane = (uint32_t)__cvta_generic_to_shared(hist) + 4u * lane;
+  const uint32_t* segw = (const uint32_t*)(seg + o * kSegStride);  // this lane's octant row, 2 voxels per word
+  const int64_t nrows = (int64_t)L[1] * L[2];
+  const int64_t nv = nrows * L[0];
   const int64_t b = blockIdx.z;
-  const int64_t v0 = blockIdx.y * slice_len;
-  const int64_t v1 = (v0 + slice_len) < nv ? (v0 + slice_len) : nv;
+  const int64_t r0 = blockIdx.y * slice_rows;
+  const int64_t r1 = (r0 + slice_rows) < nrows ? (r0 + slice_rows) : nrows;
+  const int16_t* cwb = cwo + (b * NO) * nv;
   __syncthreads();
-  // each warp: a contiguous run of voxels with incremental grid counters
-  const int64_t per = (v1 - v0 + nwarps - 1) / nwarps;
-  int64_t va = v0 + warp * per, vb = va + per < v1 ? va + per : v1;
-  if (va < vb) {
-    int x = (int)(va % L[0]), y = (int)((va / L[0]) % L[1]), z = (int)(va / ((int64_t)L[0] * L[1]));
-    const int16_t* cw = cwo + (b * nv) * NO;
-    for (int64_t v = va; v < vb; ++v) {
-      const float cx = axc[0][x], cy = axc[1][y];
-      float h = cx * s[0];
-      h = fmaf(cy, s[1], h);
-      float cz = 0.f;
-      if (ND == 3) { cz = axc[2][z]; h = fmaf(cz, s[2], h); }
-      int bin = alpha32_or_repair(h, g);
-      if (bin < 0) {
-        double h64 = __dadd_rn(__dmul_rn((double)cx, (double)s[0]), __dmul_rn((double)cy, (double)s[1]));
-        if (ND == 3) h64 = __dadd_rn(h64, __dmul_rn((double)cz, (double)s[2]));
-        bin = alpha64(h64, g);
-        note_repair();
+  for (int64_t row = r0 + warp; row < r1; row += nwarps) {
+    const int y = (int)(row % L[1]), z = (int)(row / L[1]);
+    const float cy = axc[1][y], cz = ND == 3 ? axc[2][z] : 0.f;
+    float C = cy * s[1];
+    if (ND == 3) C = fmaf(cz, s[2], C);
+    const float U0 = fmaf(fmaf(-s[0], c0 / (float)S, C), A, Bc);
+    for (int x0 = 0; x0 < L[0]; x0 += kSegVox) {
+      const int nx = (L[0] - x0) < kSegVox ? (L[0] - x0) : kSegVox;
+      // stage the segment's NO octant rows: seg[oo][0..nx)
+      const int64_t src0 = row * L[0] + x0;
+      if (((src0 | nx | nv) & 7) == 0) {
+        const int per = nx >> 3;  // uint4 per row
+        for (int t = lane; t < NO * per; t += 32) {
+          const int oo = t / per, k = t - oo * per;
+          *(uint4*)(seg + oo * kSegStride + 8 * k) = __ldg((const uint4*)(cwb + oo * nv + src0) + k);
+        }
+      } else {
+        for (int t = lane; t < NO * nx; t += 32) {
+          const int oo = t / nx, k = t - oo * nx;
+          seg[oo * kSegStride + k] = cwb[oo * nv + src0 + k];
+        }
       }
-      const int w = cw[v * NO + o];
-      if (active && w != 0) atomicAdd(&hist[lane * TS + bin], w);
-      if (++x == L[0]) { x = 0; if (++y == L[1]) { y = 0; ++z; } }
+      if (nx & 1) seg[o * kSegStride + nx] = 0;  // pad the odd tail voxel (same value by all lanes of o)
+      __syncwarp();
+      float xf = (float)x0;
+      for (int xi = 0; xi < nx; xi += 2) {
+        const uint32_t pair = active ? segw[xi >> 1] : 0u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int w = h == 0 ? (int)(int16_t)(pair & 0xFFFFu) : (int)pair >> 16;
+          const float u = fmaf(xf, a0, U0);
+          xf += 1.f;
+          int bin = __float2int_ru(u);
+          if (fabsf(u - rintf(u)) < tau) bin = grid_repair(x0 + xi + h, axc[0][x0 + xi + h], cy, cz, s, ND, gp);
+          else if (clampit) bin = bin < 0 ? 0 : (bin > Tm1 ? Tm1 : bin);
+          if (w != 0) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(hlane + 128u * (uint32_t)bin), "r"(w));
+        }
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 32 * T; i += blockDim.x) {
-    int r = i / T, q = i - r * T;
-    int val = hist[r * TS + q];
+    int q = i >> 5, r = i & 31;
+    int val = hist[i];
     if (val != 0 && blockIdx.x * 32 + r < Dc)
       atomicAdd(diff + ((b_offset + b) * Dc + blockIdx.x * 32 + r) * (int64_t)T + q, (unsigned long long)(long long)val);
   }
@@ -577,23 +623,27 @@ wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndi
   count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   const int tiles = (Dc + 31) / 32;
-  // slices: enough CTAs for >= 4 waves, each slice at most 2^18 voxels (int32 partials:
-  // 2^18 * 8 cells * 255 < 2^31)
-  int64_t slice = (int64_t)1 << 18;
+  // slices of whole rows: enough CTAs for >= 4 waves; int32 partials stay below 2^31
+  // (a CTA sees <= 2^18 voxels * 1020 |cw| per direction)
+  const int64_t L0 = ndim == 2 ? dims[1] : dims[2];
+  const int64_t nrows = nv / L0;
+  int64_t rows_cap = ((int64_t)1 << 18) / L0;
+  if (rows_cap < 1) rows_cap = 1;
   int64_t want = ((int64_t)num_sms * 8 + tiles * nb - 1) / (tiles * nb);
   if (want < 1) want = 1;
-  int64_t s2 = (nv + want - 1) / want;
-  if (s2 < slice) slice = s2 < 2048 ? 2048 : s2;
-  int64_t nslices = (nv + slice - 1) / slice;
-  const size_t smem = (size_t)32 * (T + 1) * sizeof(int);
+  int64_t slice_rows = (nrows + want - 1) / want;
+  if (slice_rows > rows_cap) slice_rows = rows_cap;
+  if (slice_rows < 1) slice_rows = 1;
+  const int64_t nslices = (nrows + slice_rows - 1) / slice_rows;
+  const size_t smem = (size_t)32 * T * sizeof(int) + (size_t)8 * (1 << ndim) * kSegStride * sizeof(int16_t);
   dim3 gridd(tiles, (unsigned)nslices, (unsigned)nb);
   MainTimer timer(st);
   if (ndim == 2) {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_grid_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_grid_hist<2><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], 1, dirs, d_begin, Dc, gp, slice, b0, diff); count_launch();
+    k_grid_hist<2><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], 1, dirs, d_begin, Dc, gp, slice_rows, b0, diff); count_launch();
   } else {
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_grid_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_grid_hist<3><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], dims[2], dirs, d_begin, Dc, gp, slice, b0, diff); count_launch();
+    k_grid_hist<3><<<gridd, 256, smem, st>>>(cwo, dims[0], dims[1], dims[2], dirs, d_begin, Dc, gp, slice_rows, b0, diff); count_launch();
   }
   timer.stop();
   WECT_CUDA_TRY(cudaGetLastError());
