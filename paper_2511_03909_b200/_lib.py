@@ -7,7 +7,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwect.so")
+LIB_PATH = os.environ.get("WECT_LIBWECT_OVERRIDE", os.path.join(HERE, "libwect.so"))  # dev experiments only
 
 # wect_status
 OK, EINVAL, ERANGE, EOVERFLOW, ECUDA, ENOMEM, ENOTSUP = 0, -1, -2, -3, -4, -5, -6

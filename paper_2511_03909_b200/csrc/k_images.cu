@@ -101,21 +101,22 @@ __global__ void k_grid_params(int ndim, int64_t d0, int64_t d1, int64_t d2, cons
 //   off[k]  : packets of four u32 byte offsets (id * 128) into the cw table, k < npk;
 //             each bin's ids are padded to whole packets with the padding row HW
 //             (whose packed value is the bias, i.e. weight 0)
-//   mask[k/32] bit k%32 : packet k ends a chunk (fold the packed sums into the totals)
-//   emit[i] : for the i-th flagged packet, the number of bins whose value is the running
-//             total after it (bin q with z empty bins after it emits 1 + z; chunk splits
-//             of bins with > kMaxRun ids emit 0; leading empty bins ride on an
-//             all-padding packet)
-// Layout per direction (u32 words): [off: 4*Lp][mask: Lp/32+1][emit: Lp (u16, padded)].
+//   meta[g]  : one byte per packet of group g (4 packets): bit 0 "end of chunk" (fold the
+//              packed sums into the running totals), bits 1..7 emit = number of bins
+//              whose value is the running total after this packet (bin q with z empty
+//              bins after it emits 1 + z; chunk splits of bins with > kMaxRun ids emit 0;
+//              leading empty bins and emits > kMaxEmit ride on all-padding packets).
+//              Loaded with the packets, so no dependent load sits on the run-end path.
 // Also records the direction's quadrant o = (s_x > 0) | (s_y > 0) << 1 in qlist.
 // ---------------------------------------------------------------------------
 constexpr int kMaxRun = 128;     // ids per chunk: 128 * 510 < 65536, no carry between packed halves
 
-__host__ __device__ constexpr int sweep_prog_packets(int HW, int T) { return (HW / 4 + T + 12) & ~3; }
-__host__ __device__ constexpr int sweep_mask_words(int HW, int T) { return sweep_prog_packets(HW, T) / 32 + 1; }
-// u32 words per direction program
+constexpr int kMaxEmit = 127;    // emit field of a packet's metadata byte
+
+__host__ __device__ constexpr int sweep_prog_packets(int HW, int T) { return (HW / 4 + T + T / kMaxEmit + 16 + 15) & ~15; }
+// u32 words per direction: [off: 4 per packet][meta: 1 per group of 4 packets]
 __host__ __device__ constexpr int sweep_prog_words(int HW, int T) {
-  return (4 * sweep_prog_packets(HW, T) + sweep_mask_words(HW, T) + (sweep_prog_packets(HW, T) + 1) / 2 + 4 + 3) & ~3;
+  return 4 * sweep_prog_packets(HW, T) + sweep_prog_packets(HW, T) / 4;
 }
 
 __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __restrict__ dirs, int d_begin, int Dc,
@@ -133,8 +134,6 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
   uint16_t* vbin = (uint16_t*)(sh + 2 * T + Lp);
   __shared__ int npk_total;
   uint32_t* off = prog + (int64_t)dl * sweep_prog_words(HW, T);
-  uint32_t* mask = off + 4 * Lp;
-  uint16_t* emitv = (uint16_t*)(mask + sweep_mask_words(HW, T));
   for (int q = threadIdx.x; q < T; q += blockDim.x) counts[q] = 0;
   for (int k = threadIdx.x; k < Lp; k += blockDim.x) meta[k] = 0;
   for (int k = threadIdx.x; k < 4 * Lp; k += blockDim.x) off[k] = (uint32_t)HW * 128u;  // padding row
@@ -153,15 +152,25 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
   if (threadIdx.x == 0) {  // serial over bins: packet bases and per-packet metadata
     int pk = 0, q = 0;
     while (q < T && counts[q] == 0) ++q;
-    if (q > 0) meta[pk++] = q | (1 << 16);  // leading empty bins (q <= T <= 4096 < 65536)
+    for (int lead = q; lead > 0;) {  // leading empty bins: all-padding packets
+      const int e = lead < kMaxEmit ? lead : kMaxEmit;
+      meta[pk++] = e | (1 << 16);
+      lead -= e;
+    }
     while (q < T) {
       int q2 = q + 1;
       while (q2 < T && counts[q2] == 0) ++q2;
       const int npk = (counts[q] + 3) / 4;
       base[q] = pk;
       for (int k = kMaxRun / 4 - 1; k < npk - 1; k += kMaxRun / 4) meta[pk + k] = 1 << 16;  // chunk split
-      meta[pk + npk - 1] = (q2 - q) | (1 << 16);
+      int emit = q2 - q;
+      int e = emit < kMaxEmit ? emit : kMaxEmit;
+      meta[pk + npk - 1] = e | (1 << 16);
       pk += npk;
+      for (emit -= e; emit > 0; emit -= e) {  // long gaps: all-padding packets
+        e = emit < kMaxEmit ? emit : kMaxEmit;
+        meta[pk++] = e | (1 << 16);
+      }
       q = q2;
     }
     pk = (pk + 3) & ~3;  // whole groups of 4 packets (the tail packets are padding, no flags)
@@ -178,18 +187,15 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
     off[4 * base[bq] + r] = (uint32_t)v * 128u;
   }
   const int npk = npk_total;
-  for (int w = threadIdx.x; w < sweep_mask_words(HW, T); w += blockDim.x) {
-    uint32_t m = 0;
-    for (int j = 0; j < 32; ++j) {
-      const int k = w * 32 + j;
-      if (k < npk && (meta[k] >> 16)) m |= 1u << j;
+  uint32_t* metaw = off + 4 * Lp;
+  for (int g = threadIdx.x; g < npk / 4; g += blockDim.x) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = meta[4 * g + j];
+      w |= (uint32_t)(((m & 0xFFFF) << 1) | (m >> 16)) << (8 * j);
     }
-    mask[w] = m;
-  }
-  if (threadIdx.x == 0) {  // emit counts of the flagged packets, in order
-    int i = 0;
-    for (int k = 0; k < npk; ++k)
-      if (meta[k] >> 16) emitv[i++] = (uint16_t)(meta[k] & 0xFFFF);
+    metaw[g] = w;
   }
 }
 
@@ -255,29 +261,33 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 // consumed four at a time: all 16 gathers are issued before the (warp-uniform)
 // end-of-chunk checks, so each warp keeps 16 shared loads in flight.
 template <typename OutT>
-__device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* __restrict__ prg, int npk,
-                                                int Lp, int nmask, int* __restrict__ st, OutT* __restrict__ out,
-                                                int64_t img0, int nimg, int Dc, int dl, int T, int lane) {
+__device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* __restrict__ prg, int npk, int Lp,
+                                                int* __restrict__ st, OutT* __restrict__ out, int64_t img0, int nimg,
+                                                int Dc, int dl, int T, int lane) {
   const uint4* pk = (const uint4*)prg;
-  const uint32_t* mask = prg + 4 * Lp;
-  const uint16_t* emitv = (const uint16_t*)(mask + nmask);
-  int q = 0, tot0 = 0, tot1 = 0, n = 0, ei = 0;
+  const uint32_t* metaw = prg + 4 * Lp;
+  int q = 0, tot0 = 0, tot1 = 0, n = 0;
   uint32_t a = 0;
-  uint32_t m = 0;
-  // software pipeline: the next group's 4 packets are loaded while this group gathers
+  // the program streams from L2: prefetch it into L1 (one 128-byte line per lane)
+  if (lane * 8 < npk) asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + lane * 8));
+  if (lane * 32 < npk / 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(metaw + lane * 32));
   uint4 w0 = __ldg(pk), w1 = __ldg(pk + 1), w2 = __ldg(pk + 2), w3 = __ldg(pk + 3);
+  uint32_t mw = __ldg(metaw);
 #pragma unroll 1
   for (int k = 0; k < npk; k += 4) {
-    if ((k & 31) == 0) m = __ldg(mask + (k >> 5));
+    if ((k & 255) == 252 && lane * 8 + k + 4 < npk)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + k + 4 + lane * 8));
     uint32_t s[4];
     s[0] = lds32(lane4 + w0.x) + lds32(lane4 + w0.y) + lds32(lane4 + w0.z) + lds32(lane4 + w0.w);
     s[1] = lds32(lane4 + w1.x) + lds32(lane4 + w1.y) + lds32(lane4 + w1.z) + lds32(lane4 + w1.w);
     s[2] = lds32(lane4 + w2.x) + lds32(lane4 + w2.y) + lds32(lane4 + w2.z) + lds32(lane4 + w2.w);
     s[3] = lds32(lane4 + w3.x) + lds32(lane4 + w3.y) + lds32(lane4 + w3.z) + lds32(lane4 + w3.w);
+    const uint32_t m = mw;
     if (k + 4 < npk) {
       w0 = __ldg(pk + k + 4); w1 = __ldg(pk + k + 5); w2 = __ldg(pk + k + 6); w3 = __ldg(pk + k + 7);
+      mw = __ldg(metaw + (k >> 2) + 1);
     }
-    if ((m & 0xFu) == 0) {  // no chunk end among these 4 packets
+    if ((m & 0x01010101u) == 0) {  // no chunk end among these 4 packets
       a += (s[0] + s[1]) + (s[2] + s[3]);
       n += 4;
     } else {
@@ -285,13 +295,13 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
       for (int j = 0; j < 4; ++j) {
         a += s[j];
         ++n;
-        if (m & (1u << j)) {
+        const uint32_t mj = (m >> (8 * j)) & 0xFFu;
+        if (mj & 1u) {
           tot0 += (int)(a & 0xFFFFu) - 4 * kBias * n;
           tot1 += (int)(a >> 16) - 4 * kBias * n;
           a = 0;
           n = 0;
-          const int emit = __ldg(emitv + ei++);
-          for (int e = 0; e < emit; ++e) {
+          for (int e = (int)(mj >> 1); e > 0; --e) {
             *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = make_int2(tot0, tot1);
             ++q;
             if ((q & (kStageBins - 1)) == 0 || q == T) {
@@ -303,7 +313,6 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
         }
       }
     }
-    m >>= 4;
   }
 }
 
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   uint32_t* cwb = (uint32_t*)smem;                 // [HW][32] words: images (2l, 2l+1) biased u16
   uint8_t* pix = smem + align16((size_t)(HW + 1) * 128);  // [HW][kPixStride] u8 (64 used)
   unsigned char* wbase = pix + sweep_pix_bytes(HW) + (size_t)(threadIdx.x >> 5) * sweep_warp_bytes(HW, T);
-  const int Lp = sweep_prog_packets(HW, T), Lw = sweep_prog_words(HW, T), nmask = sweep_mask_words(HW, T);
+  const int Lp = sweep_prog_packets(HW, T), Lw = sweep_prog_words(HW, T);
   int* st = (int*)wbase;                                             // [kStageBins][kStageStride]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lane4 = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
@@ -378,8 +387,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       __syncthreads();
       for (int k = warp; k < qco; k += kSweepWarps) {
         const int dl = qlist[o * Dc + k];
-        sweep_direction<OutT>(lane4, prog + (int64_t)dl * Lw, prog_len[dl], Lp, nmask, st, out, img0, nimg, Dc, dl,
-                              T, lane);
+        sweep_direction<OutT>(lane4, prog + (int64_t)dl * Lw, prog_len[dl], Lp, st, out, img0, nimg, Dc, dl, T, lane);
         __syncwarp();
       }
     }

@@ -1,0 +1,13 @@
+# Round profile set: bench lines + launch list + ncu --set full of each dominant kernel.
+set -x
+mkdir -p gpurun_out/prof
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > gpurun_out/prof/smi.txt
+timeout 600 python bench.py > gpurun_out/prof/bench_cfg1.json 2> gpurun_out/prof/bench_cfg1.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/prof/launches_cfg1.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+for spec in "k_sweep2d:1:2" "k_grid_hist:2:2" "k_complex:3:1" "k_ecf:ecfx:2"; do
+  k=${spec%%:*}; rest=${spec#*:}; c=${rest%%:*}; s=${rest#*:}
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $s -c 1 -o gpurun_out/prof/full_$k python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --config $c > gpurun_out/prof/full_$k.log 2>&1
+done
+for c in 0 2 3 4 ecfx; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/prof/bench_cfg$c.json 2> gpurun_out/prof/bench_cfg$c.err; done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/prof/bench_ref_cfg1.json 2>&1
+ls -la gpurun_out/prof
