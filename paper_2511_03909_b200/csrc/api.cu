@@ -96,6 +96,14 @@ static int num_sms_current() {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     cache[dev] = n > 0 ? n : 148;
+    // keep stream-ordered scratch cached across calls: with the default release threshold
+    // (0) every synchronisation hands the pool back and the next call pays cudaMalloc
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
   }
   return cache[dev];
 }

@@ -26,10 +26,10 @@ rows = list(csv.reader(io.StringIO(src)))
 h = rows[1]
 data = rows[2:]
 i_src, i_s, i_e = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-tot_s = sum(int(r[i_s]) for r in data)
-tot_e = sum(int(r[i_e]) for r in data)
+tot_s = sum(int(r[i_s] or 0) for r in data) or 1
+tot_e = sum(int(r[i_e] or 0) for r in data)
 print(f"total stall samples {tot_s}, executed warp instructions {tot_e}")
 base = int(data[0][0], 16)
-ranked = sorted(data, key=lambda r: -int(r[i_s]))[:top]
+ranked = sorted(data, key=lambda r: -int(r[i_s] or 0))[:top]
 for r in sorted(ranked, key=lambda r: int(r[0], 16)):
-    print(f"{int(r[0],16)-base:6x} exec {int(r[i_e]):>10} stall {int(r[i_s]):>6} ({100*int(r[i_s])/tot_s:4.1f}%)  {r[i_src].strip()[:80]}")
+    print(f"{int(r[0],16)-base:6x} exec {int(r[i_e] or 0):>10} stall {int(r[i_s] or 0):>6} ({100*int(r[i_s] or 0)/tot_s:4.1f}%)  {r[i_src].strip()[:80]}")
