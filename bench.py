@@ -154,6 +154,11 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     wl = workload(args.config, rank)
+    if args.D and "dirs" in wl and wl["kind"] == "complex":
+        wl["dirs"] = np.ascontiguousarray(wl["dirs"][: args.D])
+        wl["updates"] = wl["updates"] // synth.CONFIGS[int(args.config)]["D"] * args.D
+        wl["alg_bytes"] += (args.D - synth.CONFIGS[int(args.config)]["D"]) * wl["T"] * 8
+        wl["name"] += f"_D{args.D}"
     stream = torch.cuda.current_stream(dev)
 
     if wl["kind"] == "images":
@@ -395,6 +400,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--D", type=int, default=0, help="override the direction count (D-sweep of configs 3/4)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -92,6 +92,49 @@ __device__ __forceinline__ float axis_coord(int g, int L, double S) {
   return __double2float_rn(c);
 }
 
+// ---- helpers of the shared-memory histogram kernels (k_complex.cu, k_cells.cu)
+// Histogram flush into the global difference table (int64 / binary64); zeroes the rows.
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ void flush_hist(Acc* hist, int rows, int T, int TS, int row0, int Dc, void* diff) {
+  for (int i = threadIdx.x; i < rows * T; i += blockDim.x) {
+    const int r = i / T, q = i - r * T;
+    const Acc val = hist[r * TS + q];
+    if (val != (Acc)0 && row0 + r < Dc) {
+      const int64_t o = (int64_t)(row0 + r) * T + q;
+      if (FLOATW) atomicAdd((double*)diff + o, (double)val);
+      else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
+    }
+    hist[r * TS + q] = (Acc)0;
+  }
+}
+
+// Signed weight (-1)^dim w of cell b of segment S, accumulator type.
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ Acc cell_weight(const Seg& S, int64_t b) {
+  Acc w;
+  if (FLOATW) w = S.weights ? __ldg((const float*)S.weights + b) : 1.f;
+  else w = S.weights ? __ldg((const int*)S.weights + b) : 1;
+  return S.sign < 0 ? -w : w;
+}
+
+__device__ __forceinline__ int64_t chunk_cells(bool floatw, int64_t float_chunk, const unsigned int* wmax_bits,
+                                               int64_t span) {
+  // int32 partials: chunk * max|w| < 2^31; float partials are flushed every float_chunk cells
+  if (floatw) return float_chunk;
+  const unsigned int wm = *wmax_bits;
+  int64_t chunk = wm == 0 ? span : (int64_t)(2147483647u / wm);
+  return chunk < 1 ? 1 : chunk;
+}
+
+
+inline static int64_t pick_slice(int64_t total, int tiles, int per_sm, int num_sms, int64_t cap) {
+  int64_t want = ((int64_t)num_sms * per_sm * 2 + tiles - 1) / tiles;
+  int64_t slice = (total + want - 1) / want;
+  if (slice > cap) slice = cap;
+  if (slice < 256) slice = 256;
+  return slice;
+}
+
 }  // namespace wect
 
 #define WECT_CUDA_TRY(expr)                                                    \

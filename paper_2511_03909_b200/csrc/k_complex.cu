@@ -156,39 +156,6 @@ __device__ __forceinline__ void flush_hist_t(Acc* hist, int T, int row0, int Dc,
   }
 }
 
-// Histogram flush into the global difference table (int64 / binary64); zeroes the rows.
-template <bool FLOATW, typename Acc>
-__device__ __forceinline__ void flush_hist(Acc* hist, int rows, int T, int TS, int row0, int Dc, void* diff) {
-  for (int i = threadIdx.x; i < rows * T; i += blockDim.x) {
-    const int r = i / T, q = i - r * T;
-    const Acc val = hist[r * TS + q];
-    if (val != (Acc)0 && row0 + r < Dc) {
-      const int64_t o = (int64_t)(row0 + r) * T + q;
-      if (FLOATW) atomicAdd((double*)diff + o, (double)val);
-      else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
-    }
-    hist[r * TS + q] = (Acc)0;
-  }
-}
-
-// Signed weight (-1)^dim w of cell b of segment S, accumulator type.
-template <bool FLOATW, typename Acc>
-__device__ __forceinline__ Acc cell_weight(const Seg& S, int64_t b) {
-  Acc w;
-  if (FLOATW) w = S.weights ? __ldg((const float*)S.weights + b) : 1.f;
-  else w = S.weights ? __ldg((const int*)S.weights + b) : 1;
-  return S.sign < 0 ? -w : w;
-}
-
-__device__ __forceinline__ int64_t chunk_cells(bool floatw, int64_t float_chunk, const unsigned int* wmax_bits,
-                                               int64_t span) {
-  // int32 partials: chunk * max|w| < 2^31; float partials are flushed every float_chunk cells
-  if (floatw) return float_chunk;
-  const unsigned int wm = *wmax_bits;
-  int64_t chunk = wm == 0 ? span : (int64_t)(2147483647u / wm);
-  return chunk < 1 ? 1 : chunk;
-}
-
 // WECT of an explicit complex.  grid = (direction tiles of 32, cell slices); lanes =
 // directions, warps = contiguous cell streams.  Cells are taken in batches: the warp
 // first gathers a batch's vertex coordinates lane-parallel into a private smem buffer
@@ -332,166 +299,6 @@ __global__ void __launch_bounds__(256) k_complex(Segs segs, const float* __restr
   }
 }
 
-// ECF (Alg. 1 with given filters, few of them): thread per cell, a tile of up to
-// kEcfTile filters per CTA (grid.x); FVals gathered from fvals[v * m + p].  Each thread
-// takes kEcfUnroll cells of one segment per step and issues all of their index loads,
-// then all of their filter gathers, before any binning: the kernel is bound by gather
-// latency, so memory-level parallelism per thread is what matters.
-constexpr int kEcfTile = 8;
-
-__device__ __noinline__ int ecf_repair(float hmax, const GridParams* gp) {
-  note_repair();
-  return alpha64((double)hmax, *gp);  // filter values are exact in binary64
-}
-
-// Bin and count one cell (filter tile pp) -- shared by the vector and scalar paths.
-template <bool FLOATW, typename Acc>
-__device__ __forceinline__ void ecf_count(float hmax, Acc w, int pp, const GridParams& g, const GridParams* gp,
-                                          Acc* hist, int TS) {
-  const float uu = fmaf(hmax, g.A, g.B);
-  int bin = __float2int_ru(uu);
-  bin = bin < 0 ? 0 : (bin > g.T - 1 ? g.T - 1 : bin);
-  if (!g.fp32_only && fabsf(uu - rintf(uu)) < g.tau) bin = ecf_repair(hmax, gp);
-  if (w != (Acc)0) atomicAdd(&hist[pp * TS + bin], w);
-}
-
-// One segment range [b0, b1) of arity AR.  Body: each thread takes 4 consecutive cells
-// with 16-byte loads (AR int4 of indices, one of weights), then 4*AR filter gathers, so
-// every thread keeps ~4*AR+AR+1 independent loads in flight.  Scalar head / tail.
-template <bool FLOATW, int AR, typename Acc>
-__device__ __forceinline__ void ecf_segment(const Seg& S, int64_t b0, int64_t b1, int64_t k0,
-                                            const float* __restrict__ fvals, int m, int p0, int np,
-                                            const GridParams& g, const GridParams* gp, Acc* hist, int TS) {
-  auto scalar_cell = [&](int64_t b) {
-    const Acc w = cell_weight<FLOATW, Acc>(S, b);
-    int v[AR];
-    bool ok = true;
-#pragma unroll
-    for (int t = 0; t < AR; ++t) {
-      v[t] = S.verts ? __ldg(S.verts + b * AR + t) : (int)b;
-      if ((uint64_t)(int64_t)v[t] >= (uint64_t)k0) { ok = false; v[t] = 0; }
-    }
-    if (!ok) { atomicOr(&g_err_word, 1u); return; }
-    for (int pp = 0; pp < np; ++pp) {
-      float hmax = __ldg(fvals + (int64_t)v[0] * m + p0 + pp);
-#pragma unroll
-      for (int t = 1; t < AR; ++t) hmax = fmaxf(hmax, __ldg(fvals + (int64_t)v[t] * m + p0 + pp));
-      ecf_count<FLOATW, Acc>(hmax, w, pp, g, gp, hist, TS);
-    }
-  };
-  const bool vec_ok = S.verts && (((uintptr_t)S.verts & 15) == 0) && (!S.weights || ((uintptr_t)S.weights & 15) == 0);
-  int64_t vb0 = b1, vb1 = b1;
-  if (vec_ok) {
-    vb0 = (b0 + 3) & ~(int64_t)3;
-    vb1 = vb0 + ((b1 - vb0) > 0 ? ((b1 - vb0) & ~(int64_t)3) : 0);
-    if (vb0 > b1) vb0 = vb1 = b1;
-  }
-  for (int64_t b = b0 + threadIdx.x; b < (vec_ok ? vb0 : b1); b += blockDim.x) scalar_cell(b);  // head
-  for (int64_t b = vb1 + threadIdx.x; b < b1; b += blockDim.x) scalar_cell(b);                  // tail
-  for (int64_t b4 = vb0 + 4 * (int64_t)threadIdx.x; b4 < vb1; b4 += 4 * (int64_t)blockDim.x) {
-    int v[4 * AR];
-    const int4* vp = (const int4*)(S.verts + b4 * AR);
-#pragma unroll
-    for (int i = 0; i < AR; ++i) {
-      const int4 x = __ldcs(vp + i);  // streamed once: evict-first
-      v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
-    }
-    Acc w[4];
-    if (S.weights) {
-      if (FLOATW) {
-        const float4 x = __ldcs((const float4*)S.weights + (b4 >> 2));
-        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-      } else {
-        const int4 x = __ldcs((const int4*)S.weights + (b4 >> 2));
-        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-      }
-    } else {
-      w[0] = w[1] = w[2] = w[3] = (Acc)1;
-    }
-    if (S.sign < 0) { w[0] = -w[0]; w[1] = -w[1]; w[2] = -w[2]; w[3] = -w[3]; }
-    unsigned bad = 0;
-#pragma unroll
-    for (int i = 0; i < 4 * AR; ++i)
-      if ((uint64_t)(int64_t)v[i] >= (uint64_t)k0) { bad |= 1u << (i / AR); v[i] = 0; }
-    if (bad) atomicOr(&g_err_word, 1u);
-    for (int pp = 0; pp < np; ++pp) {
-      float h[4 * AR];
-#pragma unroll
-      for (int i = 0; i < 4 * AR; ++i) h[i] = __ldg(fvals + (int64_t)v[i] * m + p0 + pp);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float hmax = h[u * AR];
-#pragma unroll
-        for (int t = 1; t < AR; ++t) hmax = fmaxf(hmax, h[u * AR + t]);
-        ecf_count<FLOATW, Acc>(hmax, ((bad >> u) & 1u) ? (Acc)0 : w[u], pp, g, gp, hist, TS);
-      }
-    }
-  }
-}
-
-template <bool FLOATW>
-__global__ void __launch_bounds__(256, 3) k_ecf(Segs segs, int64_t k0, const float* __restrict__ fvals, int m,
-                                             int d_begin, int Dc, const GridParams* __restrict__ gp,
-                                             const unsigned int* __restrict__ wmax_bits, int64_t slice_len,
-                                             int64_t float_chunk, void* __restrict__ diff) {
-  using Acc = typename std::conditional<FLOATW, float, int>::type;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const GridParams g = *gp;
-  const int T = g.T, TS = T + 1;
-  Acc* hist = (Acc*)smraw;  // [kEcfTile][T+1]
-  __shared__ Seg ssegs[kMaxSegs];
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int i = 0; i < kMaxSegs; ++i) ssegs[i] = segs.s[i];
-  }
-  const int p0 = d_begin + blockIdx.x * kEcfTile;
-  const int np = (Dc - (int)blockIdx.x * kEcfTile) < kEcfTile ? (Dc - (int)blockIdx.x * kEcfTile) : kEcfTile;
-  for (int i = threadIdx.x; i < kEcfTile * TS; i += blockDim.x) hist[i] = (Acc)0;
-  const int64_t c0 = blockIdx.y * slice_len;
-  const int64_t c1 = (c0 + slice_len) < segs.total ? (c0 + slice_len) : segs.total;
-  const int64_t chunk = chunk_cells(FLOATW, float_chunk, wmax_bits, c1 - c0);
-  __syncthreads();
-  for (int64_t a0 = c0; a0 < c1; a0 += chunk) {
-    const int64_t a1 = (a0 + chunk) < c1 ? (a0 + chunk) : c1;
-    for (int sg = 0; sg < kMaxSegs; ++sg) {
-      const Seg& S = ssegs[sg];
-      const int64_t lo = a0 > S.start ? a0 : S.start;
-      const int64_t hi = a1 < S.start + S.count ? a1 : S.start + S.count;
-      if (lo >= hi) continue;
-      const int64_t b0 = lo - S.start, b1 = hi - S.start;
-      switch (S.arity) {
-        case 1: ecf_segment<FLOATW, 1>(S, b0, b1, k0, fvals, m, p0, np, g, gp, hist, TS); break;
-        case 2: ecf_segment<FLOATW, 2>(S, b0, b1, k0, fvals, m, p0, np, g, gp, hist, TS); break;
-        case 3: ecf_segment<FLOATW, 3>(S, b0, b1, k0, fvals, m, p0, np, g, gp, hist, TS); break;
-        case 4: ecf_segment<FLOATW, 4>(S, b0, b1, k0, fvals, m, p0, np, g, gp, hist, TS); break;
-        default: {  // generic arity (rare): one cell at a time
-          for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
-            const Acc w = cell_weight<FLOATW, Acc>(S, b);
-            for (int pp = 0; pp < np; ++pp) {
-              float hmax = -FLT_MAX;
-              bool bad = false;
-              for (int t = 0; t < S.arity; ++t) {
-                int v = S.verts ? __ldg(S.verts + b * S.arity + t) : (int)b;
-                if ((uint64_t)(int64_t)v >= (uint64_t)k0) { bad = true; v = 0; }
-                hmax = fmaxf(hmax, __ldg(fvals + (int64_t)v * m + p0 + pp));
-              }
-              if (bad) { atomicOr(&g_err_word, 1u); break; }
-              const float uu = fmaf(hmax, g.A, g.B);
-              int bin = __float2int_ru(uu);
-              bin = bin < 0 ? 0 : (bin > T - 1 ? T - 1 : bin);
-              if (!g.fp32_only && fabsf(uu - rintf(uu)) < g.tau) bin = ecf_repair(hmax, gp);
-              if (w != (Acc)0) atomicAdd(&hist[pp * TS + bin], w);
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    flush_hist<FLOATW, Acc>(hist, np, T, TS, blockIdx.x * kEcfTile, Dc, diff);
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------ cumsum epilogue
 // Alg. 1 line 11: one warp per row, 32-wide shuffle scan with carry.
 template <typename In, typename Out>
@@ -516,13 +323,6 @@ __global__ void k_finalize(const In* __restrict__ diff, int64_t rows, int T, Out
 }
 
 // ------------------------------------------------------------------ launchers
-static int64_t pick_slice(int64_t total, int tiles, int per_sm, int num_sms, int64_t cap) {
-  int64_t want = ((int64_t)num_sms * per_sm * 2 + tiles - 1) / tiles;
-  int64_t slice = (total + want - 1) / want;
-  if (slice > cap) slice = cap;
-  if (slice < 256) slice = 256;
-  return slice;
-}
 
 template <int N>
 static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* coords, int64_t k0, const float* dirs,
@@ -550,33 +350,17 @@ static wect_status launch_complex_n(bool floatw, const Segs& segs, const float* 
   return WECT_OK;
 }
 
-static wect_status launch_ecf(bool floatw, const Segs& segs, int64_t k0, const float* fvals, int m, int d_begin, int Dc,
-                              int T, const GridParams* gp, const unsigned int* wmax, void* diff, cudaStream_t st,
-                              int num_sms) {
-  const int tiles = (Dc + kEcfTile - 1) / kEcfTile;
-  const size_t smem = (size_t)kEcfTile * (T + 1) * 4;
-  int per_sm = (int)((220 * 1024) / (smem + 2048));
-  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
-  const int64_t slice = pick_slice(segs.total, tiles, per_sm, num_sms, (int64_t)1 << 20);
-  dim3 grid(tiles, (unsigned)((segs.total + slice - 1) / slice));
-  MainTimer timer(st);
-  if (floatw) {
-    WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ecf<true><<<grid, 256, smem, st>>>(segs, k0, fvals, m, d_begin, Dc, gp, wmax, slice, 4096, diff);
-  } else {
-    WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ecf<false><<<grid, 256, smem, st>>>(segs, k0, fvals, m, d_begin, Dc, gp, wmax, slice, 4096, diff);
-  }
-  count_launch();
-  timer.stop();
-  WECT_CUDA_TRY(cudaGetLastError());
-  return WECT_OK;
-}
+wect_status launch_cells(int mode, int n, bool floatw, const Segs& segs, int64_t k0, const float* fvals, int m,
+                         const float* coords, const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
+                         const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
+constexpr int kCellTile = 8;  // filters per CTA of the thread-per-cell kernels (k_cells.cu)
 
 wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                            const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
                            const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
-  if (mode == 1) return launch_ecf(floatw, segs, k0, fsrc, m_or_D, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
+  if (mode == 1 || Dc <= kCellTile)  // ECF, or few directions: one streaming pass, thread per cell
+    return launch_cells(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp, wmax, diff, st,
+                        num_sms);
   switch (n) {
 #define WECT_CASE(NN) \
   case NN: return launch_complex_n<NN>(floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
