@@ -320,3 +320,75 @@ def test_cfg5_scaled_float_vs_O2():
     cx, dirs, T = c["complex"], c["dirs"], c["T"]
     o2 = oracle.wect_complex(cx, dirs, T)
     assert_float_close(gpu_wect_complex(cx, dirs, T), o2, abs_cumsum(cx, dirs, T))
+
+
+def _full_M(cx, dirs):
+    """M over ALL directions (reading A2), via the oracle's heights, chunked over directions."""
+    M = 0.0
+    for a in range(0, dirs.shape[0], 64):
+        M = max(M, float(np.abs(oracle.heights(cx.coords, dirs[a:a + 64])).max()))
+    return M
+
+
+@pytest.mark.slow
+def test_cfg4_full_mesh_sampled_directions_vs_O2():
+    """BASELINE configs[3] at full size (1e7 V / 3e7 E / 2e7 F, D = 1024, T = 512) in the bench
+    launch configuration; 3 sampled rows through the oracle with the full set's M."""
+    c = synth.make_config(3)
+    cx, dirs, T = c["complex"], c["dirs"], c["T"]
+    g = gpu_wect_complex(cx, dirs, T)
+    M = _full_M(cx, dirs)
+    rows = [0, 517, 1023]
+    o2 = oracle.wect_complex(cx, np.ascontiguousarray(dirs[rows]), T, maxheight_override=M)
+    assert (g[rows] == o2).all()
+    assert (g[:, -1] == g[0, -1]).all()  # top bin = chi(K, w) in every direction
+
+
+@pytest.mark.slow
+def test_cfg5_full_complex_sampled_directions_vs_O2():
+    """BASELINE configs[4] at full size (2e6 random 4-simplices with all faces, fp32 weights,
+    D = 256, T = 256); 2 sampled rows within the A8 tolerance."""
+    c = synth.make_config(4)
+    cx, dirs, T = c["complex"], c["dirs"], c["T"]
+    g = gpu_wect_complex(cx, dirs, T)
+    M = _full_M(cx, dirs)
+    rows = [3, 200]
+    d = np.ascontiguousarray(dirs[rows])
+    o2 = oracle.wect_complex(cx, d, T, maxheight_override=M)
+    ab = synth.Complex(cx.coords, np.abs(cx.vweights), [synth.Cells(x.verts, np.abs(x.weights), 0) for x in cx.cells],
+                       cx.k0, True)
+    A = oracle.wect_complex(ab, d, T, maxheight_override=M)
+    assert_float_close(g[rows], o2, A)
+
+
+def test_images_edge_cases():
+    """1x1 images (a single vertex), B not a multiple of 64, T = 2, all-zero images."""
+    dirs = synth.directions_s1(5)
+    one = np.full((3, 1, 1), 9, np.uint8)
+    out = w.wect_images(torch.from_numpy(one).to(DEV), torch.from_numpy(dirs).to(DEV), 4).cpu().numpy()
+    assert (out == oracle.wect_images(one, dirs, 4)).all()
+    z = np.zeros((65, 6, 6), np.uint8)
+    out = w.wect_images(torch.from_numpy(z).to(DEV), torch.from_numpy(dirs).to(DEV), 2).cpu().numpy()
+    assert (out == 0).all()
+    g = np.random.default_rng(13)
+    im = g.integers(0, 256, (129, 6, 6), dtype=np.uint8)
+    out = w.wect_images(torch.from_numpy(im).to(DEV), torch.from_numpy(dirs).to(DEV), 2).cpu().numpy()
+    assert (out == oracle.wect_images(im, dirs, 2)).all()
+
+
+def test_small_D_streaming_path_vs_O2():
+    """D <= 8 goes through the thread-per-cell streaming kernel (k_cells): exact vs O2 for
+    several arities, ambient dimensions and both weight types."""
+    for seed in range(6):
+        g = np.random.default_rng(700 + seed)
+        n = int(g.integers(1, 6))
+        isf = bool(seed % 2)
+        cx = synth.random_small_complex(seed, n=n, nverts=400, ntop=300, kmax=4, float_weights=isf)
+        dirs = g.standard_normal((int(g.integers(1, 9)), n)).astype(np.float32)
+        T = int(g.choice([2, 33, 256]))
+        o2 = oracle.wect_complex(cx, dirs, T)
+        got = gpu_wect_complex(cx, dirs, T)
+        if isf:
+            assert_float_close(got, o2, abs_cumsum(cx, dirs, T))
+        else:
+            assert (got == o2).all()
