@@ -462,12 +462,17 @@ __global__ void __launch_bounds__(256) k_grid_cw(const uint8_t* __restrict__ img
 constexpr int kSegVox = 256;     // voxels per staged row segment
 constexpr int kSegStride = 264;  // int16 per staged octant row (132 words = 4 mod 32: conflict-free)
 
-__device__ __noinline__ int grid_repair(int x, float cx, float cy, float cz, const float* s, int nd,
+__device__ __noinline__ int grid_repair(float cx, float cy, float cz, float s0, float s1, float s2, int nd,
                                         const GridParams* gp) {
-  double h64 = __dadd_rn(__dmul_rn((double)cx, (double)s[0]), __dmul_rn((double)cy, (double)s[1]));
-  if (nd == 3) h64 = __dadd_rn(h64, __dmul_rn((double)cz, (double)s[2]));
+  double h64 = __dadd_rn(__dmul_rn((double)cx, (double)s0), __dmul_rn((double)cy, (double)s1));
+  if (nd == 3) h64 = __dadd_rn(h64, __dmul_rn((double)cz, (double)s2));
   note_repair();
   return alpha64(h64, *gp);
+}
+
+// predicated shared-memory add (no branch, no reconvergence barrier)
+__device__ __forceinline__ void red_shared_nz(uint32_t addr, int w) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, 0;\n\t@p red.shared.add.s32 [%0], %1;\n\t}" ::"r"(addr), "r"(w));
 }
 
 template <int ND>
@@ -507,6 +512,7 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
   const int Tm1 = T - 1;
   const uint32_t hlane = (uint32_t)__cvta_generic_to_shared(hist) + 4u * lane;
   const uint32_t* segw = (const uint32_t*)(seg + o * kSegStride);  // this lane's octant row, 2 voxels per word
+  const uint32_t amask = active ? 0xFFFFFFFFu : 0u;  // inactive lanes add nothing
   const int64_t nrows = (int64_t)L[1] * L[2];
   const int64_t nv = nrows * L[0];
   const int64_t b = blockIdx.z;
@@ -540,16 +546,17 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
       __syncwarp();
       float xf = (float)x0;
       for (int xi = 0; xi < nx; xi += 2) {
-        const uint32_t pair = active ? segw[xi >> 1] : 0u;
+        const uint32_t pair = segw[xi >> 1] & amask;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int w = h == 0 ? (int)(int16_t)(pair & 0xFFFFu) : (int)pair >> 16;
           const float u = fmaf(xf, a0, U0);
           xf += 1.f;
           int bin = __float2int_ru(u);
-          if (fabsf(u - rintf(u)) < tau) bin = grid_repair(x0 + xi + h, axc[0][x0 + xi + h], cy, cz, s, ND, gp);
+          if (__builtin_expect(fabsf(u - rintf(u)) < tau, 0))
+            bin = grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
           else if (clampit) bin = bin < 0 ? 0 : (bin > Tm1 ? Tm1 : bin);
-          if (w != 0) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(hlane + 128u * (uint32_t)bin), "r"(w));
+          red_shared_nz(hlane + 128u * (uint32_t)bin, w);
         }
       }
       __syncwarp();
