@@ -11,6 +11,7 @@
 // The paper's Theta(k m) intermediates never exist: FVals for cfg4 would be
 // 41 GB of fp32.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -354,6 +355,10 @@ wect_status launch_cells(int mode, int n, bool floatw, const Segs& segs, int64_t
                          const float* coords, const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
                          const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
 constexpr int kCellTile = 8;  // filters per CTA of the thread-per-cell kernels (k_cells.cu)
+bool vb_supported(int T);
+wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
+                              const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
+                              const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
 
 wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                            const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
@@ -361,6 +366,8 @@ wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const
   if (mode == 1 || Dc <= kCellTile)  // ECF, or few directions: one streaming pass, thread per cell
     return launch_cells(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp, wmax, diff, st,
                         num_sms);
+  if (vb_supported(T) && !getenv("WECT_DISABLE_VB"))  // vertex bins once per tile, cells from packed rows
+    return launch_complex_vb(n, floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
   switch (n) {
 #define WECT_CASE(NN) \
   case NN: return launch_complex_n<NN>(floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
