@@ -13,6 +13,7 @@
 // direction); a cell costs `arity` coalesced 128-byte row loads (L2-resident for meshes
 // stored in spatial order) and a packed max, independent of n.
 #include <cfloat>
+#include <cstdint>
 
 #include "common.cuh"
 
@@ -119,80 +120,102 @@ __device__ __forceinline__ void vb_batch(const int* ids, int nb, Acc wl, const u
   }
 }
 
+// merge a CTA's [T][2][32] histogram into the global difference table and clear it
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ void flush_tile(Acc* hist, int T, int row0, int np, void* diff) {
+  for (int i = threadIdx.x; i < T * 64; i += blockDim.x) {
+    const int q = i >> 6, col = i & 63, half = col >> 5, l = col & 31;
+    const int r = 2 * l + half;  // direction within the tile
+    const Acc val = hist[i];
+    if (val != (Acc)0 && r < np) {
+      const int64_t o = (int64_t)(row0 + r) * T + q;
+      if (FLOATW) atomicAdd((double*)diff + o, (double)val);
+      else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
+    }
+    hist[i] = (Acc)0;
+  }
+}
+
+// Work order (L2 locality): batches of kVbBatch cells of every segment advance in NSTEP
+// lock-steps; in step i each segment's batches [i U_s / NSTEP, (i+1) U_s / NSTEP) are
+// spread over all warps of the grid (grid-stride).  For a complex stored in spatial
+// order this keeps the concurrently gathered VB rows inside a narrow vertex window, so
+// each row comes from HBM about once per tile.  One histogram flush per CTA at the end
+// (the launcher checks max|w| * cells-per-CTA < 2^31 for integer weights).
 template <bool FLOATW>
 __global__ void __launch_bounds__(512) k_cells_vb(Segs segs, int64_t k0, const uint32_t* __restrict__ vb, int row0,
-                                                  int np, int Dc, const GridParams* __restrict__ gp,
-                                                  const unsigned int* __restrict__ wmax_bits, int64_t slice_len,
-                                                  int64_t float_chunk, void* __restrict__ diff) {
+                                                  int np, int Dc, const GridParams* __restrict__ gp, int nstep,
+                                                  const unsigned int* __restrict__ wmax_bits, int64_t cta_cells_step,
+                                                  void* __restrict__ diff) {
   using Acc = typename std::conditional<FLOATW, float, int>::type;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int T = gp->T;
   Acc* hist = (Acc*)smraw;  // [T][2][32]: column (half, lane) = direction 2*lane + half
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  int* ids = (int*)(smraw + (size_t)T * 64 * sizeof(Acc)) + warp * (kVbBatch * 8);  // 16 warps
+  int* ids = (int*)(smraw + (size_t)T * 64 * sizeof(Acc)) + warp * (kVbBatch * 8);
   __shared__ Seg ssegs[kMaxSegs];
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < kMaxSegs; ++i) ssegs[i] = segs.s[i];
   }
   for (int i = threadIdx.x; i < T * 64; i += blockDim.x) hist[i] = (Acc)0;
-  const int64_t c0 = blockIdx.y * slice_len;
-  const int64_t c1 = (c0 + slice_len) < segs.total ? (c0 + slice_len) : segs.total;
-  const int64_t chunk = chunk_cells(FLOATW, float_chunk, wmax_bits, c1 - c0);
   Acc* hl = hist + lane;
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, W = (int64_t)gridDim.x * nwarps;
+  // int32 partials: flush every `every` steps so that max|w| * cells since the flush < 2^31
+  int every = nstep;
+  if (!FLOATW) {
+    const unsigned int wm = *wmax_bits;
+    if (wm) {
+      const int64_t e = (int64_t)2147483647 / ((int64_t)wm * cta_cells_step);
+      every = e < 1 ? 1 : (e < nstep ? (int)e : nstep);
+    }
+  } else {  // float partials (fp32) are merged into binary64 every <= 32768 cells (reading A8)
+    const int64_t e = 32768 / (cta_cells_step > 0 ? cta_cells_step : 1);
+    every = e < 1 ? 1 : (e < nstep ? (int)e : nstep);
+  }
   __syncthreads();
-  for (int64_t a0 = c0; a0 < c1; a0 += chunk) {
-    const int64_t a1 = (a0 + chunk) < c1 ? (a0 + chunk) : c1;
-    const int64_t per = (a1 - a0 + nwarps - 1) / nwarps;
-    const int64_t w0 = a0 + warp * per, w1 = (w0 + per) < a1 ? (w0 + per) : a1;
-    int sg = 0;
-    for (int64_t c = w0; c < w1;) {
-      while (c >= ssegs[sg].start + ssegs[sg].count) ++sg;
+  for (int step = 0; step < nstep; ++step) {
+    if (step > 0 && step % every == 0) {
+      __syncthreads();
+      flush_tile<FLOATW, Acc>(hist, T, row0, np, diff);
+      __syncthreads();
+    }
+    for (int sg = 0; sg < segs.nseg; ++sg) {
       const Seg& S = ssegs[sg];
       const int ar = S.arity;
-      int nb = (kVbBatch * 8) / ar;
-      nb = nb > kVbBatch ? kVbBatch : nb;
-      const int64_t lim = S.start + S.count < w1 ? S.start + S.count : w1;
-      if (c + nb > lim) nb = (int)(lim - c);
-      const int64_t b0 = c - S.start;
-      // lane-parallel: the batch's vertex ids (coalesced) and weights
-      unsigned badcells = 0;
-      for (int t = lane; t < nb * ar; t += 32) {
-        int v = S.verts ? __ldg(S.verts + b0 * ar + t) : (int)(b0 + t);
-        if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
-        ids[t] = v;
-      }
+      int bs = (kVbBatch * 8) / ar;
+      bs = bs > kVbBatch ? kVbBatch : bs;
+      const int64_t U = (S.count + bs - 1) / bs;
+      const int64_t u0 = U * step / nstep, u1 = U * (step + 1) / nstep;
+      for (int64_t u = u0 + ((gw - u0) % W + W) % W; u < u1; u += W) {
+        const int64_t b0 = u * bs;
+        const int nb = (S.count - b0) < bs ? (int)(S.count - b0) : bs;
+        unsigned badcells = 0;
+        for (int t = lane; t < nb * ar; t += 32) {
+          int v = S.verts ? __ldg(S.verts + b0 * ar + t) : (int)(b0 + t);
+          if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
+          ids[t] = v;
+        }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) badcells |= __shfl_xor_sync(0xffffffffu, badcells, o);
-      Acc wl = (Acc)0;
-      if (lane < nb && !((badcells >> lane) & 1u)) wl = cell_weight<FLOATW, Acc>(S, b0 + lane);
-      if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
-      __syncwarp();
-      switch (ar) {
-        case 1: vb_batch<1, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-        case 2: vb_batch<2, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-        case 3: vb_batch<3, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-        case 4: vb_batch<4, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-        case 5: vb_batch<5, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-        default: vb_batch<0, FLOATW>(ids, nb, wl, vb, hl, lane, ar); break;
+        for (int o = 16; o; o >>= 1) badcells |= __shfl_xor_sync(0xffffffffu, badcells, o);
+        Acc wl = (Acc)0;
+        if (lane < nb && !((badcells >> lane) & 1u)) wl = cell_weight<FLOATW, Acc>(S, b0 + lane);
+        if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
+        __syncwarp();
+        switch (ar) {
+          case 1: vb_batch<1, FLOATW>(ids, nb, wl, vb, hl, lane); break;
+          case 2: vb_batch<2, FLOATW>(ids, nb, wl, vb, hl, lane); break;
+          case 3: vb_batch<3, FLOATW>(ids, nb, wl, vb, hl, lane); break;
+          case 4: vb_batch<4, FLOATW>(ids, nb, wl, vb, hl, lane); break;
+          case 5: vb_batch<5, FLOATW>(ids, nb, wl, vb, hl, lane); break;
+          default: vb_batch<0, FLOATW>(ids, nb, wl, vb, hl, lane, ar); break;
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      c += nb;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < T * 64; i += blockDim.x) {
-      const int q = i >> 6, col = i & 63, half = col >> 5, l = col & 31;
-      const int r = 2 * l + half;  // direction within the tile
-      const Acc val = hist[i];
-      if (val != (Acc)0 && r < np) {
-        const int64_t o = (int64_t)(row0 + r) * T + q;
-        if (FLOATW) atomicAdd((double*)diff + o, (double)val);
-        else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)val);
-      }
-      hist[i] = (Acc)0;
-    }
-    __syncthreads();
   }
+  __syncthreads();
+  flush_tile<FLOATW, Acc>(hist, T, row0, np, diff);
 }
 
 template <int N>
@@ -202,12 +225,33 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs, const float* coord
   uint32_t* vb = nullptr;
   WECT_CUDA_TRY(cudaMallocAsync((void**)&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t), st));
   const size_t smem = (size_t)T * 64 * 4 + (size_t)16 * kVbBatch * 8 * sizeof(int);
-  int per_sm = (int)((220 * 1024) / (smem + 2048));
-  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
-  const int64_t slice = pick_slice(segs.total, 1, per_sm, num_sms, (int64_t)1 << 22);
-  dim3 grid(1, (unsigned)((segs.total + slice - 1) / slice));
+  int per_sm = (int)((220 * 1024) / (smem + 1024));  // 512-thread CTAs that fit one SM's smem
+  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+  const int ctas = num_sms * per_sm;
+  // steps: every warp gets ~4 batches of EVERY segment per step (balanced, narrow window)
+  int64_t minU = INT64_MAX;
+  for (int i = 0; i < segs.nseg; ++i) {
+    if (segs.s[i].count == 0) continue;
+    int bs = (kVbBatch * 8) / segs.s[i].arity;
+    bs = bs > kVbBatch ? kVbBatch : bs;
+    const int64_t U = (segs.s[i].count + bs - 1) / bs;
+    minU = U < minU ? U : minU;
+  }
+  const int64_t per_step = (int64_t)ctas * 16 * 4;  // 4 batches per warp per segment per step
+  int nstep = minU == INT64_MAX ? 1 : (int)(minU / per_step);
+  nstep = nstep < 1 ? 1 : nstep;
   int vblocks = (int)((k0 + 255) / 256);
   vblocks = vblocks > num_sms * 8 ? num_sms * 8 : (vblocks < 1 ? 1 : vblocks);
+  // bound on the cells one CTA processes per step (for the int32 flush period)
+  int64_t cta_cells_step = 0;
+  for (int i = 0; i < segs.nseg; ++i) {
+    const int ar = segs.s[i].arity;
+    int bs = (kVbBatch * 8) / ar;
+    bs = bs > kVbBatch ? kVbBatch : bs;
+    const int64_t U = (segs.s[i].count + bs - 1) / bs;
+    const int64_t per_warp = (U / nstep + 1 + (int64_t)ctas * 16 - 1) / ((int64_t)ctas * 16);
+    cta_cells_step += 16 * per_warp * bs;
+  }
   wect_status s = WECT_OK;
   for (int t0 = 0; t0 < Dc && s == WECT_OK; t0 += kVbTile) {
     const int np = (Dc - t0) < kVbTile ? (Dc - t0) : kVbTile;
@@ -216,10 +260,10 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs, const float* coord
     MainTimer timer(st);
     if (floatw) {
       WECT_CUDA_TRY(cudaFuncSetAttribute(k_cells_vb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_cells_vb<true><<<grid, 512, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, wmax, slice, 4096, diff);
+      k_cells_vb<true><<<ctas, 512, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, nstep, wmax, cta_cells_step, diff);
     } else {
       WECT_CUDA_TRY(cudaFuncSetAttribute(k_cells_vb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_cells_vb<false><<<grid, 512, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, wmax, slice, 4096, diff);
+      k_cells_vb<false><<<ctas, 512, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, nstep, wmax, cta_cells_step, diff);
     }
     count_launch();
     timer.stop();
@@ -230,6 +274,9 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs, const float* coord
   return s;
 }
 
+// smem fits, and (integer weights) a CTA's int32 partials cannot overflow: every CTA sees at
+// most total/num_sms + one step's worth of cells, checked against the host bound on max|w|
+// (255 for the configs; callers with larger weights fall back to k_complex's chunked flush)
 bool vb_supported(int T) { return (size_t)T * 64 * 4 + (size_t)16 * kVbBatch * 8 * sizeof(int) <= 200 * 1024; }
 
 wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
