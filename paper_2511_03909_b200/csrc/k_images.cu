@@ -266,8 +266,7 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
                                                 int Dc, int dl, int T, int lane) {
   const uint4* pk = (const uint4*)prg;
   const uint32_t* metaw = prg + 4 * Lp;
-  int q = 0, tot0 = 0, tot1 = 0, n = 0;
-  uint32_t a = 0;
+  int q = 0, tot0 = 0, tot1 = 0;
   // the program streams from L2: prefetch it into L1 (one 128-byte line per lane)
   if (lane * 8 < npk) asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + lane * 8));
   if (lane * 32 < npk / 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(metaw + lane * 32));
@@ -287,32 +286,28 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
       w0 = __ldg(pk + k + 4); w1 = __ldg(pk + k + 5); w2 = __ldg(pk + k + 6); w3 = __ldg(pk + k + 7);
       mw = __ldg(metaw + (k >> 2) + 1);
     }
-    if ((m & 0x01010101u) == 0) {  // no chunk end among these 4 packets
-      a += (s[0] + s[1]) + (s[2] + s[3]);
-      n += 4;
-    } else {
+    // every packet carries exactly 4 biased loads: fold it straight into the int32 totals
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        a += s[j];
-        ++n;
-        const uint32_t mj = (m >> (8 * j)) & 0xFFu;
-        if (mj & 1u) {
-          tot0 += (int)(a & 0xFFFFu) - 4 * kBias * n;
-          tot1 += (int)(a >> 16) - 4 * kBias * n;
-          a = 0;
-          n = 0;
-          for (int e = (int)(mj >> 1); e > 0; --e) {
-            *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = make_int2(tot0, tot1);
-            ++q;
-            if ((q & (kStageBins - 1)) == 0 || q == T) {
-              __syncwarp();
-              sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, (q - 1) & ~(kStageBins - 1), lane);
-              __syncwarp();
-            }
+    for (int j = 0; j < 4; ++j) {
+      tot0 += (int)(s[j] & 0xFFFFu) - 4 * kBias;
+      tot1 += (int)(s[j] >> 16) - 4 * kBias;
+      const uint32_t mj = (m >> (8 * j)) & 0xFEu;  // emit count (bit 0, the fold, is implicit now)
+      if (mj) {
+        for (int e = (int)(mj >> 1); e > 0; --e) {
+          *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = make_int2(tot0, tot1);
+          if (((++q) & (kStageBins - 1)) == 0) {
+            __syncwarp();
+            sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q - kStageBins, lane);
+            __syncwarp();
           }
         }
       }
     }
+  }
+  if (q & (kStageBins - 1)) {  // the last, partial chunk (T not a multiple of 8)
+    __syncwarp();
+    sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q & ~(kStageBins - 1), lane);
+    __syncwarp();
   }
 }
 
