@@ -151,7 +151,7 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2511_03909_b200 as w
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     wl = workload(args.config, rank)
     if args.D and "dirs" in wl and wl["kind"] == "complex":
@@ -414,8 +414,9 @@ def main():
     if world > 1:
         import torch
 
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
+        torch.cuda.set_device(dev)
+        torch.distributed.init_process_group("nccl", device_id=dev)
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
