@@ -356,6 +356,9 @@ wect_status launch_cells(int mode, int n, bool floatw, const Segs& segs, int64_t
                          const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
 constexpr int kCellTile = 8;  // filters per CTA of the thread-per-cell kernels (k_cells.cu)
 bool vb_supported(int T);
+wect_status launch_stream(int mode, int n, bool floatw, const Segs& segs, int64_t k0, const float* fvals, int m,
+                          const float* coords, const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
+                          const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
 wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                               const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
                               const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
@@ -363,9 +366,13 @@ wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float*
 wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                            const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
                            const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
-  if (mode == 1 || Dc <= kCellTile)  // ECF, or few directions: one streaming pass, thread per cell
+  if (mode == 1 || Dc <= kCellTile) {  // ECF, or few directions: one streaming pass, thread per cell
+    const wect_status s = launch_stream(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp,
+                                        wmax, diff, st, num_sms);
+    if (s != WECT_ENOTSUP) return s;
     return launch_cells(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp, wmax, diff, st,
                         num_sms);
+  }
   if (vb_supported(T) && !getenv("WECT_DISABLE_VB"))  // vertex bins once per tile, cells from packed rows
     return launch_complex_vb(n, floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
   switch (n) {

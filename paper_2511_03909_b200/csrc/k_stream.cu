@@ -1,0 +1,497 @@
+// k_stream.cu -- the HBM-bound end of the explicit-complex path: the ECF (ecf_complex,
+// the ECF-X row) and the WECT at few directions (D <= 8, SURVEY 8(d) D-sweep).
+// Alg. 1 with one cell per thread-iteration: gather the filter values of the
+// cell's vertices (MODE 0: FVals[v, p]; MODE 1: <coords[v], s_p> by fp32 FMA), take the
+// max (eq. msi: alpha is monotone, so the bin of the max height is the max of the vertex
+// bins), bin it (reading A1: fp32 + guard, binary64 repair), and add the signed weight into
+// a shared-memory histogram (line 9); k_finalize does the cumsum (line 11).
+//
+// B200 shape: a persistent CTA per SM.  A producer warp streams the index lists and
+// weights of 1920-cell units HBM -> shared memory with cp.async.bulk into a 3-stage ring
+// (mbarrier complete_tx), so HBM latency is covered by the ring instead of by thread
+// occupancy; 15 consumer warps read their cells' ids from shared memory, release the
+// stage at once, then gather (L2-resident filter values / coordinates), bin and count.
+// Histogram [p][bin][R]: R lane replicas (R = 32 when it fits) so that lanes of a warp
+// hitting the same bin -- the common case for spatially coherent heights -- never
+// collide in a shared-memory bank.  Units are dealt round-robin over the CTAs, so the
+// units in flight at any moment are adjacent in the cell lists (gathers stay in L2).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace wect {
+
+constexpr int kStreamConsumers = 15;  // consumer warps (+ the producer: 4 warps per SM sub-partition)
+constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);  // + 1 producer warp
+constexpr int kStreamStages = 3;
+constexpr int kStreamMaxAr = 5;
+constexpr int kStreamUnit = 4 * 32 * kStreamConsumers;  // 1920 cells (arity <= 4; 960 for arity 5)
+constexpr int kStreamIdxBytes = kStreamUnit * 4 * 4;
+constexpr int kStreamWBytes = kStreamUnit * 4;
+constexpr int kStreamTile = 8;                 // filters per CTA (grid.y tiles)
+constexpr int kStreamHistBytes = 64 * 1024;
+
+struct StreamUnits {
+  int64_t ustart[kMaxSegs + 1];  // first unit of each segment (prefix sum)
+};
+
+__host__ __device__ constexpr int stream_unit_cells(int ar) { return ar <= 4 ? kStreamUnit : kStreamUnit / 2; }
+
+// ---- mbarrier / bulk-copy PTX (sm_90+; CTA-local, no cluster)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// L2 policy for the streamed index lists and weights: read once, so evict first -- the
+// gathered filter values / coordinates (re-read by every cell dimension) keep the L2.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+// a pointer the compiler cannot re-associate with the 32-bit offsets added to it
+__device__ __forceinline__ const float* opaque(const float* p) {
+  const float* q;
+  asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
+  return q;
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kStreamConsumers)); }
+
+__device__ __noinline__ int stream_ecf_repair(float hmax, const GridParams* gp) {
+  note_repair();
+  return alpha64((double)hmax, *gp);  // filter values are exact in binary64
+}
+
+template <int AR>
+struct CellIds {
+  int v[AR];
+};
+
+template <int N, int AR>
+__device__ __noinline__ int stream_wect_repair(const CellIds<AR> ids, const float* __restrict__ coords,
+                                               const float* s, const GridParams* gp) {
+  double hm = -DBL_MAX;
+  for (int t = 0; t < AR; ++t) {
+    const float* x = coords + (int64_t)ids.v[t] * N;
+    double h = __dmul_rn((double)x[0], (double)s[0]);
+    for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x[i], (double)s[i]));
+    hm = fmax(hm, h);
+  }
+  note_repair();
+  return alpha64(hm, *gp);
+}
+
+template <int MODE, int N, bool FLOATW>
+struct StreamCtx {
+  using Acc = typename std::conditional<FLOATW, float, int>::type;
+  const float* fv;      // MODE 0: fvals + p0
+  int m;                // MODE 0: row stride of fvals
+  const float* coords;  // MODE 1
+  const float* sdir;    // MODE 1: [np][N] in shared memory
+  int np, T, rl, rmask, row0;
+  bool direct;  // int weights too large for int32 partials: add straight into the int64 table
+  uint32_t k0c;
+  void* diff;
+  GridParams g;
+  const GridParams* gp;
+  Acc* hist;
+};
+
+__device__ __noinline__ void stream_add_direct(void* diff, int64_t o, int w) {
+  atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)w);
+}
+
+// KG cells (ids v[KG][AR], already validated; dead cells carry weight 0 and vertex 0):
+// every gather of the group is issued before any binning, then one shared-memory atomic
+// per (cell, filter).  Near-edge cells are repaired after the fast pass (rare calls).
+template <int MODE, int N, bool FLOATW, int AR, int KG>
+__device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c, const int (*v)[AR],
+                                             const typename StreamCtx<MODE, N, FLOATW>::Acc* w, int lane) {
+  if constexpr (MODE == 0) {
+    for (int pp = 0; pp < c.np; ++pp) {
+      const float* fp = opaque(c.fv + pp);  // keeps each gather one IMAD.WIDE.U32 off the base
+      float h[KG][AR];
+#pragma unroll
+      for (int k = 0; k < KG; ++k)
+#pragma unroll
+        for (int t = 0; t < AR; ++t) h[k][t] = __ldg(fp + (uint32_t)v[k][t] * (uint32_t)c.m);  // k0*m < 2^32
+      float hm[KG];
+      int bin[KG];
+      unsigned near = 0;
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        hm[k] = h[k][0];
+#pragma unroll
+        for (int t = 1; t < AR; ++t) hm[k] = fmaxf(hm[k], h[k][t]);
+        const float uu = fmaf(hm[k], c.g.A, c.g.B);
+        const int b = __float2int_ru(uu);
+        bin[k] = max(0, min(b, c.T - 1));
+        near |= (fabsf(uu - rintf(uu)) < c.g.tau ? 1u : 0u) << k;
+      }
+      if (__builtin_expect(near != 0 && !c.g.fp32_only, 0)) {
+#pragma unroll
+        for (int k = 0; k < KG; ++k)
+          if ((near >> k) & 1u) bin[k] = stream_ecf_repair(hm[k], c.gp);
+      }
+      if (!FLOATW && c.direct) {
+#pragma unroll
+        for (int k = 0; k < KG; ++k) stream_add_direct(c.diff, (int64_t)(c.row0 + pp) * c.T + bin[k], (int)w[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < KG; ++k) atomicAdd(c.hist + (((pp * c.T + bin[k]) << c.rl) | (lane & c.rmask)), w[k]);
+      }
+    }
+  } else {
+    float x[KG][AR * N];
+    const float* cb = opaque(c.coords);
+#pragma unroll
+    for (int k = 0; k < KG; ++k)
+#pragma unroll
+      for (int t = 0; t < AR; ++t) {
+        const float* xv = cb + (uint32_t)v[k][t] * (uint32_t)N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[k][t * N + i] = __ldg(xv + i);
+      }
+    for (int pp = 0; pp < c.np; ++pp) {
+      const float* s = c.sdir + pp * N;
+      float sv[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) sv[i] = s[i];
+      int bin[KG];
+      unsigned near = 0;
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        float hmax = -FLT_MAX;
+#pragma unroll
+        for (int t = 0; t < AR; ++t) {
+          float h = x[k][t * N] * sv[0];
+#pragma unroll
+          for (int i = 1; i < N; ++i) h = fmaf(x[k][t * N + i], sv[i], h);
+          hmax = fmaxf(hmax, h);
+        }
+        const float uu = fmaf(hmax, c.g.A, c.g.B);
+        const int b = __float2int_ru(uu);
+        bin[k] = max(0, min(b, c.T - 1));
+        near |= (fabsf(uu - rintf(uu)) < c.g.tau ? 1u : 0u) << k;
+      }
+      if (__builtin_expect(near != 0 && !c.g.fp32_only, 0)) {
+#pragma unroll
+        for (int k = 0; k < KG; ++k)
+          if ((near >> k) & 1u) {
+            CellIds<AR> ids;
+#pragma unroll
+            for (int t = 0; t < AR; ++t) ids.v[t] = v[k][t];
+            bin[k] = stream_wect_repair<N, AR>(ids, c.coords, s, c.gp);
+          }
+      }
+      if (!FLOATW && c.direct) {
+#pragma unroll
+        for (int k = 0; k < KG; ++k) stream_add_direct(c.diff, (int64_t)(c.row0 + pp) * c.T + bin[k], (int)w[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < KG; ++k) atomicAdd(c.hist + (((pp * c.T + bin[k]) << c.rl) | (lane & c.rmask)), w[k]);
+      }
+    }
+  }
+}
+
+// Consume one unit of `cells` cells (arity AR) of segment S starting at cell b0; its ids
+// and weights are all in the stage (the producer stores a segment's last <= 3 ids /
+// weights itself, which a 16-byte bulk copy cannot carry).  Releases the stage (one
+// arrive per warp) as soon as the ids are in registers.
+template <int MODE, int N, bool FLOATW, int AR>
+__device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c, const Seg S, int64_t b0, int cells,
+                                            const int* sid, const void* sw, uint64_t* empty, int ctid, int lane) {
+  using Acc = typename StreamCtx<MODE, N, FLOATW>::Acc;
+  constexpr int CPT = stream_unit_cells(AR) / (32 * kStreamConsumers);  // cells per thread: 4 or 2
+  constexpr int KG = (CPT * AR * (MODE == 0 ? 1 : N) <= 40) ? CPT : ((CPT / 2) * AR * (MODE == 0 ? 1 : N) <= 40 ? CPT / 2 : 1);
+  int v[CPT][AR];
+  Acc w[CPT];
+  unsigned bad = 0;
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int cl = ctid + k * 32 * kStreamConsumers;  // strided: conflict-free shared loads
+    if (S.verts) {
+      const int* p = sid + cl * AR;
+      if constexpr (AR == 4) {
+        const int4 q = *(const int4*)p;
+        v[k][0] = q.x; v[k][1] = q.y; v[k][2] = q.z; v[k][3] = q.w;
+      } else if constexpr (AR == 2) {
+        const int2 q = *(const int2*)p;
+        v[k][0] = q.x; v[k][1] = q.y;
+      } else {
+#pragma unroll
+        for (int t = 0; t < AR; ++t) v[k][t] = p[t];
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < AR; ++t) v[k][t] = (int)(b0 + cl);
+    }
+    const Acc wk = S.weights ? ((const Acc*)sw)[cl] : (Acc)1;
+    w[k] = S.sign < 0 ? -wk : wk;
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);  // stage free for the producer
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int cl = ctid + k * 32 * kStreamConsumers;
+    bool ok = cl < cells, oob = false;
+#pragma unroll
+    for (int t = 0; t < AR; ++t) oob |= (uint32_t)v[k][t] >= c.k0c;
+    bad |= (ok && oob) ? 1u : 0u;
+    ok = ok && !oob;
+    if (!ok) {
+      w[k] = (Acc)0;
+#pragma unroll
+      for (int t = 0; t < AR; ++t) v[k][t] = 0;
+    }
+  }
+  if (bad) atomicOr(&g_err_word, 1u);
+#pragma unroll
+  for (int k0 = 0; k0 < CPT; k0 += KG) stream_group<MODE, N, FLOATW, AR, KG>(c, v + k0, w + k0, lane);
+}
+
+template <bool FLOATW, typename Acc>
+__device__ __forceinline__ void stream_flush(Acc* hist, int np, int T, int rl, int row0, int Dc, void* diff,
+                                             int ctid) {
+  const int R = 1 << rl;
+  for (int i = ctid; i < np * T; i += 32 * kStreamConsumers) {
+    Acc s = (Acc)0;
+    for (int r = 0; r < R; ++r) {
+      const int j = (i << rl) + ((r + i) & (R - 1));  // rotated: lanes hit distinct banks
+      s += hist[j];
+      hist[j] = (Acc)0;
+    }
+    const int p = i / T, q = i - p * T;
+    if (s != (Acc)0 && row0 + p < Dc) {
+      const int64_t o = (int64_t)(row0 + p) * T + q;
+      if (FLOATW) atomicAdd((double*)diff + o, (double)s);
+      else atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)s);
+    }
+  }
+}
+
+template <int MODE, int N, bool FLOATW>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    k_stream(Segs segs, StreamUnits su, int64_t k0, const float* __restrict__ fvals, int m,
+             const float* __restrict__ coords, const float* __restrict__ dirs, int d_begin, int Dc,
+             const GridParams* __restrict__ gp, int rl, const unsigned int* __restrict__ wmax_bits,
+             int64_t float_chunk, void* __restrict__ diff) {
+  using Acc = typename std::conditional<FLOATW, float, int>::type;
+  constexpr int NS = N > 0 ? N : 1;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned char* sidx = smraw;                                        // [stages][kStreamIdxBytes]
+  unsigned char* sw = smraw + kStreamStages * kStreamIdxBytes;        // [stages][kStreamWBytes]
+  Acc* hist = (Acc*)(sw + kStreamStages * kStreamWBytes);            // [np][T][R]
+  __shared__ __align__(8) uint64_t full[kStreamStages], empty[kStreamStages];
+  __shared__ Seg ssegs[kMaxSegs];
+  __shared__ int64_t sustart[kMaxSegs + 1];
+  __shared__ float sdir[kStreamTile * NS];
+
+  const GridParams g = *gp;
+  const int T = g.T, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.y, p0 = d_begin + tile * kStreamTile;
+  const int np = (Dc - tile * kStreamTile) < kStreamTile ? (Dc - tile * kStreamTile) : kStreamTile;
+  const int R = 1 << rl;
+  if (tid < kMaxSegs) ssegs[tid] = segs.s[tid];
+  if (tid <= kMaxSegs) sustart[tid] = su.ustart[tid];
+  if (MODE == 1)
+    for (int i = tid; i < np * NS; i += blockDim.x) sdir[i] = dirs[(int64_t)p0 * NS + i];
+  for (int i = tid; i < np * T * R; i += blockDim.x) hist[i] = (Acc)0;
+  if (tid == 0) {
+    for (int s = 0; s < kStreamStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kStreamConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t nunits = sustart[segs.nseg];
+  const int64_t G = gridDim.x;
+  const int64_t my_units = nunits > blockIdx.x ? (nunits - blockIdx.x + G - 1) / G : 0;
+  // unit j of this CTA = global unit blockIdx.x + j*G; its segment and cell range
+  auto locate = [&](int64_t u, int& sg, int64_t& b0, int& cells) {
+    sg = 0;
+    while (sg + 1 < segs.nseg && u >= sustart[sg + 1]) ++sg;
+    const int uc = stream_unit_cells(ssegs[sg].arity);
+    b0 = (u - sustart[sg]) * uc;
+    const int64_t rem = ssegs[sg].count - b0;
+    cells = rem < uc ? (int)rem : uc;
+  };
+
+  if (warp == kStreamConsumers) {  // ---- producer warp
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first();
+      for (int64_t j = 0; j < my_units; ++j) {
+        const int st = (int)(j % kStreamStages);
+        if (j >= kStreamStages) mbar_wait(&empty[st], (unsigned)(((j / kStreamStages) - 1) & 1));
+        int sg, cells;
+        int64_t b0;
+        locate(blockIdx.x + j * G, sg, b0, cells);
+        const Seg& S = ssegs[sg];
+        const unsigned ib = S.verts ? (unsigned)(((int64_t)cells * S.arity * 4) & ~15ll) : 0u;
+        const unsigned wb = S.weights ? (unsigned)(((int64_t)cells * 4) & ~15ll) : 0u;
+        // a segment's last 1..3 ids / weights: plain stores, published by the arrive below
+        const int ni = S.verts ? cells * S.arity : 0;
+        for (int t = (int)(ib >> 2); t < ni; ++t)
+          ((int*)(sidx + st * kStreamIdxBytes))[t] = __ldg(S.verts + b0 * S.arity + t);
+        if (S.weights)
+          for (int t = (int)(wb >> 2); t < cells; ++t)
+            ((int*)(sw + st * kStreamWBytes))[t] = __ldg((const int*)S.weights + b0 + t);
+        mbar_arrive_expect_tx(&full[st], ib + wb);
+        if (ib) bulk_g2s(sidx + st * kStreamIdxBytes, S.verts + b0 * S.arity, ib, &full[st], pol);
+        if (wb) bulk_g2s(sw + st * kStreamWBytes, (const char*)S.weights + b0 * 4, wb, &full[st], pol);
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  StreamCtx<MODE, NS, FLOATW> c;
+  c.fv = MODE == 0 ? fvals + p0 : nullptr;
+  c.m = m;
+  c.coords = coords;
+  c.sdir = sdir;
+  c.np = np;
+  c.T = T;
+  c.rl = rl;
+  c.rmask = R - 1;
+  c.k0c = k0 > 0x80000000ll ? 0x80000000u : (uint32_t)k0;
+  c.g = g;
+  c.gp = gp;
+  c.hist = hist;
+  c.row0 = tile * kStreamTile;
+  c.diff = diff;
+  c.direct = false;
+  // flush period (units): int32 partials below 2^31 (device max|w|); float every float_chunk cells
+  int64_t every_cells;
+  if (FLOATW) every_cells = float_chunk;
+  else {
+    const unsigned wm = *wmax_bits;
+    every_cells = wm == 0 ? ((int64_t)1 << 62) : (int64_t)(2147483647u / wm);
+    c.direct = every_cells < 2048;  // a unit alone could overflow an int32 partial
+  }
+  int64_t since = 0;
+  for (int64_t j = 0; j < my_units; ++j) {
+    const int st = (int)(j % kStreamStages);
+    int sg, cells;
+    int64_t b0;
+    locate(blockIdx.x + j * G, sg, b0, cells);
+    const Seg S = ssegs[sg];
+    if (since + cells > every_cells) {  // uniform across consumer threads
+      consumers_sync();
+      stream_flush<FLOATW, Acc>(hist, np, T, rl, tile * kStreamTile, Dc, diff, tid);
+      consumers_sync();
+      since = 0;
+    }
+    since += cells;
+    mbar_wait(&full[st], (unsigned)((j / kStreamStages) & 1));
+    const int* sid = (const int*)(sidx + st * kStreamIdxBytes);
+    const void* swp = sw + st * kStreamWBytes;
+    switch (S.arity) {
+#define WECT_AR(A)                                                                                         \
+  case A:                                                                                                  \
+    stream_unit<MODE, NS, FLOATW, A>(c, S, b0, cells, sid, swp, &empty[st], tid, lane); \
+    break;
+      WECT_AR(1) WECT_AR(2) WECT_AR(3) WECT_AR(4) WECT_AR(5)
+#undef WECT_AR
+    }
+  }
+  consumers_sync();
+  stream_flush<FLOATW, Acc>(hist, np, T, rl, tile * kStreamTile, Dc, diff, tid);
+}
+
+// Host side.  Returns WECT_ENOTSUP when the streaming kernel does not apply (an arity above
+// kStreamMaxAr, a misaligned list, or a histogram that does not fit); the caller then
+// uses k_cells.
+template <int MODE, int N>
+static wect_status launch_stream_t(bool floatw, const Segs& segs, const StreamUnits& su, int64_t k0,
+                                   const float* fvals, int m, const float* coords, const float* dirs, int d_begin,
+                                   int Dc, int T, int rl, const GridParams* gp, const unsigned int* wmax, void* diff,
+                                   cudaStream_t st, int num_sms) {
+  const int tiles = (Dc + kStreamTile - 1) / kStreamTile;
+  const int np = Dc < kStreamTile ? Dc : kStreamTile;
+  const size_t smem = (size_t)kStreamStages * (kStreamIdxBytes + kStreamWBytes) + ((size_t)np * T * 4 << rl);
+  int per_tile = num_sms / tiles;
+  per_tile = per_tile < 1 ? 1 : per_tile;
+  const int64_t nunits = su.ustart[segs.nseg];
+  if (per_tile > nunits) per_tile = (int)(nunits > 0 ? nunits : 1);
+  dim3 grid((unsigned)per_tile, (unsigned)tiles);
+  MainTimer timer(st);
+  if (floatw) {
+    auto k = k_stream<MODE, N, true>;
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, kStreamThreads, smem, st>>>(segs, su, k0, fvals, m, coords, dirs, d_begin, Dc, gp, rl, wmax, 8192,
+                                          diff);
+  } else {
+    auto k = k_stream<MODE, N, false>;
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, kStreamThreads, smem, st>>>(segs, su, k0, fvals, m, coords, dirs, d_begin, Dc, gp, rl, wmax, 8192,
+                                          diff);
+  }
+  count_launch();
+  timer.stop();
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_stream(int mode, int n, bool floatw, const Segs& segs, int64_t k0, const float* fvals, int m,
+                          const float* coords, const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
+                          const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
+  if (getenv("WECT_DISABLE_STREAM")) return WECT_ENOTSUP;
+  if ((uint64_t)k0 * (uint64_t)(mode == 1 ? m : n) >= ((uint64_t)1 << 32)) return WECT_ENOTSUP;  // 32-bit offsets
+  StreamUnits su;
+  su.ustart[0] = 0;
+  for (int i = 0; i < segs.nseg; ++i) {
+    const Seg& S = segs.s[i];
+    if (S.arity < 1 || S.arity > kStreamMaxAr) return WECT_ENOTSUP;
+    if (S.verts && ((uintptr_t)S.verts & 15)) return WECT_ENOTSUP;
+    if (S.weights && ((uintptr_t)S.weights & 15)) return WECT_ENOTSUP;
+    const int uc = stream_unit_cells(S.arity);
+    su.ustart[i + 1] = su.ustart[i] + (S.count + uc - 1) / uc;
+  }
+  for (int i = segs.nseg + 1; i <= kMaxSegs; ++i) su.ustart[i] = su.ustart[segs.nseg];
+  // histogram replicas: the largest R <= 32 with np * T * R * 4 <= 64 KB
+  const int np = Dc < kStreamTile ? Dc : kStreamTile;
+  if ((size_t)np * T * 4 > (size_t)kStreamHistBytes) return WECT_ENOTSUP;
+  int rl = 0;
+  while (rl < 5 && ((size_t)np * T * 4 << (rl + 1)) <= (size_t)kStreamHistBytes) ++rl;
+  if (mode == 1)
+    return launch_stream_t<0, 0>(floatw, segs, su, k0, fvals, m, nullptr, nullptr, d_begin, Dc, T, rl, gp, wmax, diff,
+                                 st, num_sms);
+  switch (n) {
+#define WECT_CASE(NN)                                                                                          \
+  case NN:                                                                                                     \
+    return launch_stream_t<1, NN>(floatw, segs, su, k0, nullptr, 0, coords, dirs, d_begin, Dc, T, rl, gp, wmax, \
+                                  diff, st, num_sms);
+    WECT_CASE(2) WECT_CASE(3) WECT_CASE(4) WECT_CASE(5)
+#undef WECT_CASE
+  }
+  return WECT_ENOTSUP;  // other n: k_cells
+}
+
+}  // namespace wect

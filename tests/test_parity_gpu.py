@@ -392,3 +392,44 @@ def test_small_D_streaming_path_vs_O2():
             assert_float_close(got, o2, abs_cumsum(cx, dirs, T))
         else:
             assert (got == o2).all()
+
+
+def _misaligned(a: np.ndarray) -> torch.Tensor:
+    """Device copy of `a` whose data pointer is 4 bytes past a 16-byte boundary."""
+    flat = torch.zeros(a.size + 4, dtype=torch.from_numpy(a[:0]).dtype, device=DEV)
+    view = flat[1:1 + a.size].view(a.shape)
+    view.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    assert view.data_ptr() % 16 == 4
+    return view
+
+
+def test_stream_kernel_mid_size_vs_O2():
+    """The bulk-copy ring kernel (k_stream) over enough 2048-cell units to wrap its stages
+    many times per CTA, segment tails not a multiple of 4 ids, ECF and D <= 8 WECT; the
+    int64 direct path for huge integer weights; the misaligned-list fallback (k_cells)."""
+    cx = synth.torus_mesh(601, 799, 11)  # k0 odd: every segment ends in a ragged tail
+    g = np.random.default_rng(41)
+    cells = cells_of(cx)
+    vw = torch.from_numpy(cx.vweights).to(DEV)
+    f = g.uniform(-1, 1, (cx.k0, 2)).astype(np.float32)
+    out = w.ecf_complex(torch.from_numpy(f).to(DEV), cells, 512, vweights=vw).cpu().numpy()
+    assert (out == oracle.ecf_complex(cx, f, 512)).all()
+    dirs = synth.directions_sphere(3, 3, 5)
+    o2 = oracle.wect_complex(cx, dirs, 300)
+    assert (gpu_wect_complex(cx, dirs, 300) == o2).all()
+    # misaligned index lists: same result through the fallback kernel
+    mis = [(_misaligned(np.asarray(c.verts, np.int32)), torch.from_numpy(c.weights).to(DEV), c.dim) for c in cx.cells]
+    got = w.wect_complex(torch.from_numpy(cx.coords).to(DEV), mis, torch.from_numpy(dirs).to(DEV), 300, vweights=vw)
+    assert (got.cpu().numpy() == o2).all()
+    # |w| up to 2^30: int32 partials cannot hold a unit, adds go straight to int64
+    big = synth.Complex(cx.coords, g.integers(-2**30, 2**30, cx.k0, dtype=np.int32),
+                        [synth.Cells(c.verts, g.integers(-2**30, 2**30, len(c.verts), dtype=np.int32), c.dim)
+                         for c in cx.cells], cx.k0)
+    assert (gpu_wect_complex(big, dirs[:1], 64) == oracle.wect_complex(big, dirs[:1], 64)).all()
+
+
+def test_stream_kernel_float_arity5_vs_O2():
+    cx = synth.random_simplicial(20000, 30000, 4, 4, 77, float_weights=True)  # arities 1..5
+    dirs = synth.directions_sphere(5, 4, 3)
+    T = 200
+    assert_float_close(gpu_wect_complex(cx, dirs, T), oracle.wect_complex(cx, dirs, T), abs_cumsum(cx, dirs, T))
