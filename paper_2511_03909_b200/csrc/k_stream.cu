@@ -7,7 +7,7 @@
 // a shared-memory histogram (line 9); k_finalize does the cumsum (line 11).
 //
 // B200 shape: a persistent CTA per SM.  A producer warp streams the index lists and
-// weights of 1920-cell units HBM -> shared memory with cp.async.bulk into a 3-stage ring
+// weights of 1920-cell units HBM -> shared memory with cp.async.bulk into a 4-stage ring
 // (mbarrier complete_tx), so HBM latency is covered by the ring instead of by thread
 // occupancy; 15 consumer warps read their cells' ids from shared memory, release the
 // stage at once, then gather (L2-resident filter values / coordinates), bin and count.
@@ -23,7 +23,7 @@ namespace wect {
 
 constexpr int kStreamConsumers = 15;  // consumer warps (+ the producer: 4 warps per SM sub-partition)
 constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);  // + 1 producer warp
-constexpr int kStreamStages = 3;
+constexpr int kStreamStages = 4;
 constexpr int kStreamMaxAr = 5;
 constexpr int kStreamUnit = 4 * 32 * kStreamConsumers;  // 1920 cells (arity <= 4; 960 for arity 5)
 constexpr int kStreamIdxBytes = kStreamUnit * 4 * 4;
@@ -334,8 +334,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   const int64_t G = gridDim.x;
   const int64_t my_units = nunits > blockIdx.x ? (nunits - blockIdx.x + G - 1) / G : 0;
   // unit j of this CTA = global unit blockIdx.x + j*G; its segment and cell range
+  // (units only grow along a CTA's sequence, so each caller keeps a segment cursor sg)
   auto locate = [&](int64_t u, int& sg, int64_t& b0, int& cells) {
-    sg = 0;
     while (sg + 1 < segs.nseg && u >= sustart[sg + 1]) ++sg;
     const int uc = stream_unit_cells(ssegs[sg].arity);
     b0 = (u - sustart[sg]) * uc;
@@ -346,10 +346,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   if (warp == kStreamConsumers) {  // ---- producer warp
     if (lane == 0) {
       const uint64_t pol = l2_evict_first();
+      int sg = 0;
       for (int64_t j = 0; j < my_units; ++j) {
         const int st = (int)(j % kStreamStages);
         if (j >= kStreamStages) mbar_wait(&empty[st], (unsigned)(((j / kStreamStages) - 1) & 1));
-        int sg, cells;
+        int cells;
         int64_t b0;
         locate(blockIdx.x + j * G, sg, b0, cells);
         const Seg& S = ssegs[sg];
@@ -396,9 +397,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     c.direct = every_cells < 2048;  // a unit alone could overflow an int32 partial
   }
   int64_t since = 0;
+  int sg = 0;
   for (int64_t j = 0; j < my_units; ++j) {
     const int st = (int)(j % kStreamStages);
-    int sg, cells;
+    int cells;
     int64_t b0;
     locate(blockIdx.x + j * G, sg, b0, cells);
     const Seg S = ssegs[sg];
