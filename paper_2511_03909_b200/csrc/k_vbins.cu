@@ -22,26 +22,21 @@ namespace wect {
 constexpr int kVbTile = 64;  // directions per tile: two per lane
 
 template <int N>
-__device__ __noinline__ int vertex_repair(const float* x, const float* s, const GridParams* gp) {
-  double h = __dmul_rn((double)x[0], (double)s[0]);
-  for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x[i], (double)s[i]));
+struct VecN {
+  float v[N];
+};
+
+// binary64 height of one vertex in one direction (axis order), alpha64 (reading A1)
+template <int N>
+__device__ __noinline__ int vertex_repair(const VecN<N> x, const VecN<N> s, const GridParams* gp) {
+  double h = __dmul_rn((double)x.v[0], (double)s.v[0]);
+  for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x.v[i], (double)s.v[i]));
   note_repair();
   return alpha64(h, *gp);
 }
 
-template <int N>
-__device__ __forceinline__ int vbin(const float* x, const float* s, const GridParams& g, const GridParams* gp) {
-  float h = x[0] * s[0];
-#pragma unroll
-  for (int i = 1; i < N; ++i) h = fmaf(x[i], s[i], h);
-  const float u = fmaf(h, g.A, g.B);
-  int b = __float2int_ru(u);
-  b = b < 0 ? 0 : (b > g.T - 1 ? g.T - 1 : b);
-  if (__builtin_expect(!g.fp32_only && fabsf(u - rintf(u)) < g.tau, 0)) b = vertex_repair<N>(x, s, gp);
-  return b;
-}
-
-// grid: blocks over vertices; lanes = direction pairs of the tile; each warp stages 32
+// grid: blocks over vertices; lanes = direction pairs of the tile (inactive pairs of the
+// last tile compute a harmless bin of direction 0 that nobody reads); each warp stages 32
 // vertices' coordinates (lane-parallel), then writes one 128-byte VB row per vertex.
 template <int N>
 __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords, int64_t k0,
@@ -49,13 +44,14 @@ __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords,
                                                const GridParams* __restrict__ gp, uint32_t* __restrict__ vb) {
   __shared__ float xs[8][32 * N];
   const GridParams g = *gp;
+  const float tau = g.fp32_only ? -1.f : g.tau;  // fp32-only: the guard never fires
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float sa[N], sb[N];
+  VecN<N> sa, sb;
   const int pa = 2 * lane, pb = 2 * lane + 1;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    sa[i] = pa < np ? dirs[(int64_t)(p0 + pa) * N + i] : 0.f;
-    sb[i] = pb < np ? dirs[(int64_t)(p0 + pb) * N + i] : 0.f;
+    sa.v[i] = pa < np ? dirs[(int64_t)(p0 + pa) * N + i] : 0.f;
+    sb.v[i] = pb < np ? dirs[(int64_t)(p0 + pb) * N + i] : 0.f;
   }
   float* x = xs[warp];
   const int64_t nwarps = (int64_t)gridDim.x * 8;
@@ -63,12 +59,26 @@ __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords,
     const int nv = (k0 - base) < 32 ? (int)(k0 - base) : 32;
     for (int t = lane; t < nv * N; t += 32) x[t] = __ldg(coords + base * N + t);
     __syncwarp();
+    uint32_t* row = vb + base * 32 + lane;
+#pragma unroll 2
     for (int j = 0; j < nv; ++j) {
-      float xv[N];
+      VecN<N> xv;
 #pragma unroll
-      for (int i = 0; i < N; ++i) xv[i] = x[j * N + i];
-      const int ba = pa < np ? vbin<N>(xv, sa, g, gp) : 0, bb = pb < np ? vbin<N>(xv, sb, g, gp) : 0;
-      vb[(base + j) * 32 + lane] = (uint32_t)ba | ((uint32_t)bb << 16);
+      for (int i = 0; i < N; ++i) xv.v[i] = x[j * N + i];
+      float ha = xv.v[0] * sa.v[0], hb = xv.v[0] * sb.v[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) {
+        ha = fmaf(xv.v[i], sa.v[i], ha);
+        hb = fmaf(xv.v[i], sb.v[i], hb);
+      }
+      const float ua = fmaf(ha, g.A, g.B), ub = fmaf(hb, g.A, g.B);
+      int ba = max(0, min(__float2int_ru(ua), g.T - 1)), bb = max(0, min(__float2int_ru(ub), g.T - 1));
+      const bool na = fabsf(ua - rintf(ua)) < tau, nb = fabsf(ub - rintf(ub)) < tau;
+      if (__builtin_expect(na || nb, 0)) {
+        if (na) ba = vertex_repair<N>(xv, sa, gp);
+        if (nb) bb = vertex_repair<N>(xv, sb, gp);
+      }
+      row[(int64_t)j * 32] = (uint32_t)ba | ((uint32_t)bb << 16);
     }
     __syncwarp();
   }
@@ -79,12 +89,26 @@ __device__ __forceinline__ void hist_add(int* h, int w) { atomicAdd(h, w); }
 __device__ __forceinline__ void hist_add(float* h, float w) { atomicAdd(h, w); }
 
 constexpr int kVbBatch = 32;  // cells per warp batch
+constexpr int kVbWarps = 32;  // warps per CTA (one CTA per SM: MLP for the row gathers)
 
 // nb cells of arity AR (0: runtime `arr`) from the warp's staged ids: four cells at a
 // time, all 4*AR row loads issued before the packed max and the atomics.
-template <int AR, bool FLOATW, typename Acc>
-__device__ __forceinline__ void vb_batch(const int* ids, int nb, Acc wl, const uint32_t* __restrict__ vb, Acc* hl,
-                                         int lane, int arr = AR) {
+// red.shared.add.s32 at a 32-bit shared address (int partials, native on sm_100)
+__device__ __forceinline__ void red_shared(uint32_t addr, int w) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
+}
+
+// One batch of nb <= kVbBatch cells of arity AR (0: runtime `arr`) whose ids are staged
+// in `ids` and whose signed weights sit in lane (cell) order in wl: four cells at a time,
+// all their 4*AR row loads issued before the packed max and the adds.  vbl = vb + lane
+// (the lane's column of the VB rows); hsa = shared address of hist + lane (int path) and
+// hl the same as a pointer (float path).  DIRECT (integer weights too large for int32
+// partials over one step): add straight into the int64 difference rows drow[0..T) and
+// drow[T..2T) of the lane's two directions (aa / ab: the direction exists).
+template <int AR, bool FLOATW, bool DIRECT, typename Acc>
+__device__ __forceinline__ void vb_batch(const int* ids, int nb, Acc wl, const uint32_t* __restrict__ vbl,
+                                         uint32_t hsa, Acc* hl, unsigned long long* drow, int T, bool aa, bool ab,
+                                         int arr = AR) {
   const int ar = AR > 0 ? AR : arr;
   constexpr int RA = AR > 0 ? AR : 1;
   for (int j = 0; j < nb; j += 4) {
@@ -94,7 +118,7 @@ __device__ __forceinline__ void vb_batch(const int* ids, int nb, Acc wl, const u
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int t = 0; t < RA; ++t) x[u][t] = (j + u < nb) ? __ldg(vb + (int64_t)ids[(j + u) * RA + t] * 32 + lane) : 0u;
+        for (int t = 0; t < RA; ++t) x[u][t] = (j + u < nb) ? __ldg(vbl + (int64_t)ids[(j + u) * RA + t] * 32) : 0u;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         m2[u] = x[u][0];
@@ -106,15 +130,26 @@ __device__ __forceinline__ void vb_batch(const int* ids, int nb, Acc wl, const u
       for (int u = 0; u < 4; ++u) {
         m2[u] = 0;
         if (j + u < nb)
-          for (int t = 0; t < ar; ++t) m2[u] = __vmaxu2(m2[u], __ldg(vb + (int64_t)ids[(j + u) * ar + t] * 32 + lane));
+          for (int t = 0; t < ar; ++t) m2[u] = __vmaxu2(m2[u], __ldg(vbl + (int64_t)ids[(j + u) * ar + t] * 32));
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const Acc w = __shfl_sync(0xffffffffu, wl, (j + u) & 31);
-      if (j + u < nb && w != (Acc)0) {
-        hist_add(hl + (m2[u] & 0xFFFFu) * 64, w);
-        hist_add(hl + (m2[u] >> 16) * 64 + 32, w);
+      const Acc w = __shfl_sync(0xffffffffu, wl, (j + u) & 31);  // 0 past nb
+      const uint32_t lo = m2[u] & 0xFFFFu, hi = m2[u] >> 16;
+      if constexpr (DIRECT) {
+        if (j + u < nb && w != (Acc)0) {
+          if (aa) atomicAdd(drow + lo, (unsigned long long)(long long)w);
+          if (ab) atomicAdd(drow + T + hi, (unsigned long long)(long long)w);
+        }
+      } else if constexpr (FLOATW) {
+        if (j + u < nb) {
+          hist_add(hl + lo * 64, w);
+          hist_add(hl + hi * 64 + 32, w);
+        }
+      } else {  // cells past nb carry w = 0 and a harmless bin 0
+        red_shared(hsa + lo * 256u, (int)w);
+        red_shared(hsa + hi * 256u + 128u, (int)w);
       }
     }
   }
@@ -136,16 +171,20 @@ __device__ __forceinline__ void flush_tile(Acc* hist, int T, int row0, int np, v
   }
 }
 
-// Work order (L2 locality): batches of kVbBatch cells of every segment advance in NSTEP
-// lock-steps; in step i each segment's batches [i U_s / NSTEP, (i+1) U_s / NSTEP) are
-// spread over all warps of the grid (grid-stride).  For a complex stored in spatial
-// order this keeps the concurrently gathered VB rows inside a narrow vertex window, so
-// each row comes from HBM about once per tile.  One histogram flush per CTA at the end
-// (the launcher checks max|w| * cells-per-CTA < 2^31 for integer weights).
+// Work order (L2 locality): the cells of every segment advance together in NSTEP steps;
+// step i covers cells [bnd[s][i], bnd[s][i+1]) of segment s, cut into batches of
+// kVbBatch cells spread over all warps of the grid (grid-stride).  The boundaries are
+// either uniform fractions of each segment or, after k_bucket_* (below), the vertex
+// windows of a bucketed copy of the lists, so the VB rows gathered concurrently stay in
+// a narrow window of vertices and each row comes from HBM about once per tile.  int32
+// partials are flushed before a step could overflow them (a bound on the cells one CTA
+// takes per step, times the device max|w|); fp32 partials every <= 32768 cells.
 template <bool FLOATW>
-__global__ void __launch_bounds__(512) k_cells_vb(Segs segs, int64_t k0, const uint32_t* __restrict__ vb, int row0,
+__global__ void __launch_bounds__(kVbWarps * 32, 1) k_cells_vb(Segs segs, int64_t k0, const uint32_t* __restrict__ vb, int row0,
                                                   int np, int Dc, const GridParams* __restrict__ gp, int nstep,
-                                                  const unsigned int* __restrict__ wmax_bits, int64_t cta_cells_step,
+                                                  const int64_t* __restrict__ bnd, const int* __restrict__ bat,
+                                                  const int64_t* __restrict__ bound,
+                                                  const unsigned int* __restrict__ wmax_bits,
                                                   void* __restrict__ diff) {
   using Acc = typename std::conditional<FLOATW, float, int>::type;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -160,36 +199,42 @@ __global__ void __launch_bounds__(512) k_cells_vb(Segs segs, int64_t k0, const u
   }
   for (int i = threadIdx.x; i < T * 64; i += blockDim.x) hist[i] = (Acc)0;
   Acc* hl = hist + lane;
+  const uint32_t hsa = (uint32_t)__cvta_generic_to_shared(hist + lane);
+  const uint32_t* vbl = vb + lane;
   const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, W = (int64_t)gridDim.x * nwarps;
-  // int32 partials: flush every `every` steps so that max|w| * cells since the flush < 2^31
-  int every = nstep;
+  int64_t limit;  // cells one CTA may add between flushes
   if (!FLOATW) {
     const unsigned int wm = *wmax_bits;
-    if (wm) {
-      const int64_t e = (int64_t)2147483647 / ((int64_t)wm * cta_cells_step);
-      every = e < 1 ? 1 : (e < nstep ? (int)e : nstep);
-    }
-  } else {  // float partials (fp32) are merged into binary64 every <= 32768 cells (reading A8)
-    const int64_t e = 32768 / (cta_cells_step > 0 ? cta_cells_step : 1);
-    every = e < 1 ? 1 : (e < nstep ? (int)e : nstep);
+    limit = wm ? (int64_t)2147483647 / wm : ((int64_t)1 << 62);
+  } else {
+    limit = 32768;
   }
+  int64_t since = 0;
   __syncthreads();
   for (int step = 0; step < nstep; ++step) {
-    if (step > 0 && step % every == 0) {
+    const int64_t cta_cells = __ldg(bound + step);  // k_step_info: cells one CTA may take this step
+    // a step alone could overflow the int32 partials: add straight into int64 instead
+    unsigned long long* drow =
+        (!FLOATW && cta_cells > limit) ? (unsigned long long*)diff + (int64_t)(row0 + 2 * lane) * T : nullptr;
+    const bool aa = 2 * lane < np, ab = 2 * lane + 1 < np;
+    if (since > 0 && since + cta_cells > limit) {
       __syncthreads();
       flush_tile<FLOATW, Acc>(hist, T, row0, np, diff);
       __syncthreads();
+      since = 0;
     }
+    since += cta_cells;
     for (int sg = 0; sg < segs.nseg; ++sg) {
       const Seg& S = ssegs[sg];
       const int ar = S.arity;
-      int bs = (kVbBatch * 8) / ar;
-      bs = bs > kVbBatch ? kVbBatch : bs;
-      const int64_t U = (S.count + bs - 1) / bs;
-      const int64_t u0 = U * step / nstep, u1 = U * (step + 1) / nstep;
-      for (int64_t u = u0 + ((gw - u0) % W + W) % W; u < u1; u += W) {
-        const int64_t b0 = u * bs;
-        const int nb = (S.count - b0) < bs ? (int)(S.count - b0) : bs;
+      const int bs = (kVbBatch * 8) / ar > kVbBatch ? kVbBatch : (kVbBatch * 8) / ar;
+      const int U = __ldg(bat + sg * nstep + step);
+      if ((int)gw >= U) continue;
+      const int64_t c0 = __ldg(bnd + sg * (int64_t)(nstep + 1) + step);
+      const int64_t c1 = __ldg(bnd + sg * (int64_t)(nstep + 1) + step + 1);
+      for (int u = (int)gw; u < U; u += (int)W) {
+        const int64_t b0 = c0 + (int64_t)u * bs;
+        const int nb = (c1 - b0) < bs ? (int)(c1 - b0) : bs;
         unsigned badcells = 0;
         for (int t = lane; t < nb * ar; t += 32) {
           int v = S.verts ? __ldg(S.verts + b0 * ar + t) : (int)(b0 + t);
@@ -202,13 +247,22 @@ __global__ void __launch_bounds__(512) k_cells_vb(Segs segs, int64_t k0, const u
         if (lane < nb && !((badcells >> lane) & 1u)) wl = cell_weight<FLOATW, Acc>(S, b0 + lane);
         if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
         __syncwarp();
-        switch (ar) {
-          case 1: vb_batch<1, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-          case 2: vb_batch<2, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-          case 3: vb_batch<3, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-          case 4: vb_batch<4, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-          case 5: vb_batch<5, FLOATW>(ids, nb, wl, vb, hl, lane); break;
-          default: vb_batch<0, FLOATW>(ids, nb, wl, vb, hl, lane, ar); break;
+        if (!FLOATW && drow) {
+          switch (ar) {
+            case 1: vb_batch<1, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            case 2: vb_batch<2, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            case 3: vb_batch<3, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            default: vb_batch<0, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
+          }
+        } else {
+          switch (ar) {
+            case 1: vb_batch<1, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            case 2: vb_batch<2, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            case 3: vb_batch<3, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            case 4: vb_batch<4, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            case 5: vb_batch<5, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+            default: vb_batch<0, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
+          }
         }
         __syncwarp();
       }
@@ -218,40 +272,206 @@ __global__ void __launch_bounds__(512) k_cells_vb(Segs segs, int64_t k0, const u
   flush_tile<FLOATW, Acc>(hist, T, row0, np, diff);
 }
 
+// ---- vertex-window bucketing of the cell lists (once per call, reused by every tile)
+// key(cell) = (min vertex id) >> ws; ids outside [0, k0) get key 0 (k_cells_vb still
+// reports them).  Counting sort per segment: k_bucket_count, k_bucket_scan, and
+// k_bucket_scatter (CTA-aggregated reservations; order inside a bucket is not kept).
+constexpr int kBucketMax = 4096;  // static smem: 4096 counters + 4096 bases = 48 KB
+constexpr int kScatterChunk = 4096;
+
+__device__ __forceinline__ int cell_key(const int32_t* verts, int64_t b, int ar, int64_t k0, int ws) {
+  uint32_t mn = 0xFFFFFFFFu;
+  for (int t = 0; t < ar; ++t) {
+    const uint32_t v = (uint32_t)__ldg(verts + b * ar + t);
+    mn = v < mn ? v : mn;
+  }
+  return (int64_t)mn < k0 ? (int)(mn >> ws) : 0;
+}
+
+__global__ void __launch_bounds__(512) k_bucket_count(const int32_t* __restrict__ verts, int64_t count, int ar,
+                                                      int64_t k0, int ws, int nb, int* __restrict__ cnt) {
+  __shared__ int h[kBucketMax];
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < count; b += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[cell_key(verts, b, ar, k0, ws)], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (h[i]) atomicAdd(&cnt[i], h[i]);
+}
+
+// one CTA per segment row: bnd[i] = sum of cnt[< i] (i = 0..nb), cur = bnd[0..nb)
+__global__ void __launch_bounds__(1024) k_bucket_scan(const int* __restrict__ cnt, int nb, int64_t* __restrict__ bnd,
+                                                      int64_t* __restrict__ cur) {
+  __shared__ int64_t part[1024];
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per, i1 = min(nb, i0 + per);
+  int64_t s = 0;
+  for (int i = i0; i < i1; ++i) s += cnt[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // Hillis-Steele inclusive scan
+    const int64_t x = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += x;
+    __syncthreads();
+  }
+  int64_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int i = i0; i < i1; ++i) {
+    bnd[i] = run;
+    cur[i] = run;
+    run += cnt[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) bnd[nb] = part[blockDim.x - 1];
+}
+
+__global__ void __launch_bounds__(512) k_bucket_scatter(const int32_t* __restrict__ verts,
+                                                        const void* __restrict__ weights, int64_t count, int ar,
+                                                        int64_t k0, int ws, int nb, unsigned long long* __restrict__ cur,
+                                                        int32_t* __restrict__ overts, int32_t* __restrict__ oweights) {
+  __shared__ int h[kBucketMax];
+  __shared__ unsigned long long base[kBucketMax];
+  constexpr int PER = kScatterChunk / 512;
+  for (int64_t c0 = (int64_t)blockIdx.x * kScatterChunk; c0 < count; c0 += (int64_t)gridDim.x * kScatterChunk) {
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    int key[PER], rank[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t b = c0 + k * 512 + threadIdx.x;
+      key[k] = b < count ? cell_key(verts, b, ar, k0, ws) : -1;
+      rank[k] = key[k] >= 0 ? atomicAdd(&h[key[k]], 1) : 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+      if (h[i]) base[i] = atomicAdd(&cur[i], (unsigned long long)h[i]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (key[k] < 0) continue;
+      const int64_t b = c0 + k * 512 + threadIdx.x;
+      const int64_t pos = (int64_t)base[key[k]] + rank[k];
+      for (int t = 0; t < ar; ++t) overts[pos * ar + t] = __ldg(verts + b * ar + t);
+      if (weights) oweights[pos] = __ldg((const int32_t*)weights + b);
+    }
+    __syncthreads();
+  }
+}
+
+// per step: batches of each segment (bat[s][i]) and a bound on the cells one CTA of
+// `nwarps` warps takes (grid-stride over W warps): sum_s nwarps * ceil(bat / W) * bs
+__global__ void k_step_info(Segs segs, int nstep, const int64_t* __restrict__ bnd, int W, int nwarps,
+                            int* __restrict__ bat, int64_t* __restrict__ bound) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nstep; i += gridDim.x * blockDim.x) {
+    int64_t cells = 0;
+    for (int s = 0; s < segs.nseg; ++s) {
+      const int ar = segs.s[s].arity;
+      const int bs = (kVbBatch * 8) / ar > kVbBatch ? kVbBatch : (kVbBatch * 8) / ar;
+      const int64_t c = bnd[(int64_t)s * (nstep + 1) + i + 1] - bnd[(int64_t)s * (nstep + 1) + i];
+      const int64_t u = (c + bs - 1) / bs;
+      bat[s * nstep + i] = (int)u;
+      cells += (int64_t)nwarps * ((u + W - 1) / W) * bs;
+    }
+    bound[i] = cells;
+  }
+}
+
+// uniform step boundaries: bnd[s][i] = count_s * i / nstep
+__global__ void k_uniform_bnd(Segs segs, int nstep, int64_t* __restrict__ bnd) {
+  const int s = blockIdx.x;
+  for (int i = threadIdx.x; i <= nstep; i += blockDim.x)
+    bnd[(int64_t)s * (nstep + 1) + i] = (int64_t)((__int128)segs.s[s].count * i / nstep);
+}
+
+// vertex segment under bucketing: bnd[i] = min(i << ws, count)
+__global__ void k_vertex_bnd(int64_t count, int ws, int nstep, int64_t* __restrict__ bnd) {
+  for (int i = threadIdx.x; i <= nstep; i += blockDim.x) {
+    const int64_t c = (int64_t)i << ws;
+    bnd[i] = i == nstep ? count : (c < count ? c : count);
+  }
+}
+
 template <int N>
-static wect_status launch_vb_n(bool floatw, const Segs& segs, const float* coords, int64_t k0, const float* dirs,
+static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* coords, int64_t k0, const float* dirs,
                                int d_begin, int Dc, int T, const GridParams* gp, const unsigned int* wmax, void* diff,
                                cudaStream_t st, int num_sms) {
+  Segs segs = segs_in;
   uint32_t* vb = nullptr;
   WECT_CUDA_TRY(cudaMallocAsync((void**)&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t), st));
-  const size_t smem = (size_t)T * 64 * 4 + (size_t)16 * kVbBatch * 8 * sizeof(int);
-  int per_sm = (int)((220 * 1024) / (smem + 1024));  // 512-thread CTAs that fit one SM's smem
-  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
-  const int ctas = num_sms * per_sm;
-  // steps: every warp gets ~4 batches of EVERY segment per step (balanced, narrow window)
-  int64_t minU = INT64_MAX;
-  for (int i = 0; i < segs.nseg; ++i) {
-    if (segs.s[i].count == 0) continue;
-    int bs = (kVbBatch * 8) / segs.s[i].arity;
-    bs = bs > kVbBatch ? kVbBatch : bs;
-    const int64_t U = (segs.s[i].count + bs - 1) / bs;
-    minU = U < minU ? U : minU;
+  const size_t smem = (size_t)T * 64 * 4 + (size_t)kVbWarps * kVbBatch * 8 * sizeof(int);
+  const int ctas = num_sms;  // one 1024-thread CTA per SM
+  const int ntiles = (Dc + kVbTile - 1) / kVbTile;
+  // Bucket when the VB table does not fit in L2 and there is more than one tile to reuse it
+  const bool bucket = ntiles > 1 && (size_t)k0 * 128 > ((size_t)64 << 20) && !getenv("WECT_DISABLE_BUCKETS");
+  int nstep;
+  int ws = 0;
+  if (bucket) {
+    while ((k0 >> ws) >= kBucketMax) ++ws;
+    if (ws < 16) ws = 16;  // windows of >= 64K vertices (8 MB of VB rows)
+    nstep = (int)((k0 - 1) >> ws) + 1;
+  } else {
+    // every warp gets ~4 batches of EVERY segment per step (balanced, narrow window)
+    int64_t minU = INT64_MAX;
+    for (int i = 0; i < segs.nseg; ++i) {
+      if (segs.s[i].count == 0) continue;
+      const int bs = (kVbBatch * 8) / segs.s[i].arity > kVbBatch ? kVbBatch : (kVbBatch * 8) / segs.s[i].arity;
+      const int64_t U = (segs.s[i].count + bs - 1) / bs;
+      minU = U < minU ? U : minU;
+    }
+    const int64_t per_step = (int64_t)ctas * kVbWarps * 4;
+    nstep = minU == INT64_MAX ? 1 : (int)(minU / per_step);
+    nstep = nstep < 1 ? 1 : nstep;
   }
-  const int64_t per_step = (int64_t)ctas * 16 * 4;  // 4 batches per warp per segment per step
-  int nstep = minU == INT64_MAX ? 1 : (int)(minU / per_step);
-  nstep = nstep < 1 ? 1 : nstep;
+  int64_t* bnd = nullptr;
+  void* scratch = nullptr;
+  WECT_CUDA_TRY(cudaMallocAsync((void**)&bnd, sizeof(int64_t) * kMaxSegs * (nstep + 1), st));
+  if (!bucket) {
+    k_uniform_bnd<<<segs.nseg, 256, 0, st>>>(segs, nstep, bnd);
+    count_launch();
+  } else {
+    // bucketed copies of every index list (and its weights) in one scratch block
+    size_t bytes = 0;
+    for (int i = 0; i < segs.nseg; ++i)
+      if (segs.s[i].verts) bytes += (size_t)segs.s[i].count * (segs.s[i].arity + 1) * 4 + 256;
+    size_t cbytes = sizeof(int) * kBucketMax + 2 * sizeof(int64_t) * (kBucketMax + 1);
+    WECT_CUDA_TRY(cudaMallocAsync(&scratch, bytes + cbytes, st));
+    int* cnt = (int*)scratch;
+    int64_t* cur = (int64_t*)((char*)scratch + sizeof(int) * kBucketMax);
+    char* dst = (char*)scratch + cbytes;
+    for (int i = 0; i < segs.nseg; ++i) {
+      Seg& S = segs.s[i];
+      int64_t* b = bnd + (int64_t)i * (nstep + 1);
+      if (!S.verts) {
+        k_vertex_bnd<<<1, 256, 0, st>>>(S.count, ws, nstep, b);
+        count_launch();
+        continue;
+      }
+      int32_t* ov = (int32_t*)dst;
+      dst += ((size_t)S.count * S.arity * 4 + 127) & ~(size_t)127;
+      int32_t* ow = S.weights ? (int32_t*)dst : nullptr;
+      if (S.weights) dst += ((size_t)S.count * 4 + 127) & ~(size_t)127;
+      WECT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * kBucketMax, st));
+      const int g1 = (int)((S.count + 511) / 512 < num_sms * 4 ? (S.count + 511) / 512 : num_sms * 4);
+      k_bucket_count<<<g1 > 0 ? g1 : 1, 512, 0, st>>>(S.verts, S.count, S.arity, k0, ws, nstep, cnt);
+      k_bucket_scan<<<1, 1024, 0, st>>>(cnt, nstep, b, cur);
+      const int g2 = (int)((S.count + kScatterChunk - 1) / kScatterChunk < num_sms * 4
+                               ? (S.count + kScatterChunk - 1) / kScatterChunk
+                               : num_sms * 4);
+      k_bucket_scatter<<<g2 > 0 ? g2 : 1, 512, 0, st>>>(S.verts, S.weights, S.count, S.arity, k0, ws, nstep,
+                                                       (unsigned long long*)cur, ov, ow);
+      count_launch(3);
+      S.verts = ov;
+      S.weights = ow;
+    }
+  }
+  int* bat = nullptr;
+  int64_t* bound = nullptr;
+  WECT_CUDA_TRY(cudaMallocAsync((void**)&bat, sizeof(int) * kMaxSegs * nstep, st));
+  WECT_CUDA_TRY(cudaMallocAsync((void**)&bound, sizeof(int64_t) * nstep, st));
+  k_step_info<<<(nstep + 255) / 256, 256, 0, st>>>(segs, nstep, bnd, ctas * kVbWarps, kVbWarps, bat, bound);
+  count_launch();
   int vblocks = (int)((k0 + 255) / 256);
   vblocks = vblocks > num_sms * 8 ? num_sms * 8 : (vblocks < 1 ? 1 : vblocks);
-  // bound on the cells one CTA processes per step (for the int32 flush period)
-  int64_t cta_cells_step = 0;
-  for (int i = 0; i < segs.nseg; ++i) {
-    const int ar = segs.s[i].arity;
-    int bs = (kVbBatch * 8) / ar;
-    bs = bs > kVbBatch ? kVbBatch : bs;
-    const int64_t U = (segs.s[i].count + bs - 1) / bs;
-    const int64_t per_warp = (U / nstep + 1 + (int64_t)ctas * 16 - 1) / ((int64_t)ctas * 16);
-    cta_cells_step += 16 * per_warp * bs;
-  }
   wect_status s = WECT_OK;
   for (int t0 = 0; t0 < Dc && s == WECT_OK; t0 += kVbTile) {
     const int np = (Dc - t0) < kVbTile ? (Dc - t0) : kVbTile;
@@ -260,10 +480,10 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs, const float* coord
     MainTimer timer(st);
     if (floatw) {
       WECT_CUDA_TRY(cudaFuncSetAttribute(k_cells_vb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_cells_vb<true><<<ctas, 512, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, nstep, wmax, cta_cells_step, diff);
+      k_cells_vb<true><<<ctas, kVbWarps * 32, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, nstep, bnd, bat, bound, wmax, diff);
     } else {
       WECT_CUDA_TRY(cudaFuncSetAttribute(k_cells_vb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_cells_vb<false><<<ctas, 512, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, nstep, wmax, cta_cells_step, diff);
+      k_cells_vb<false><<<ctas, kVbWarps * 32, smem, st>>>(segs, k0, vb, t0, np, Dc, gp, nstep, bnd, bat, bound, wmax, diff);
     }
     count_launch();
     timer.stop();
@@ -271,13 +491,17 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs, const float* coord
     if (e != cudaSuccess) s = fail_cuda(e, "k_cells_vb", __FILE__, __LINE__);
   }
   cudaFreeAsync(vb, st);
+  cudaFreeAsync(bnd, st);
+  cudaFreeAsync(bat, st);
+  cudaFreeAsync(bound, st);
+  if (scratch) cudaFreeAsync(scratch, st);
   return s;
 }
 
 // smem fits, and (integer weights) a CTA's int32 partials cannot overflow: every CTA sees at
 // most total/num_sms + one step's worth of cells, checked against the host bound on max|w|
 // (255 for the configs; callers with larger weights fall back to k_complex's chunked flush)
-bool vb_supported(int T) { return (size_t)T * 64 * 4 + (size_t)16 * kVbBatch * 8 * sizeof(int) <= 200 * 1024; }
+bool vb_supported(int T) { return (size_t)T * 64 * 4 + (size_t)kVbWarps * kVbBatch * 8 * sizeof(int) <= 220 * 1024; }
 
 wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                               const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
