@@ -44,6 +44,17 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# Shared-memory int32 atomic throughput (lane-ops per clock per SM, conflict-free), measured
+# with tools/microbench/smem_ubench.cu on a B200.  The ALU-side roofline
+# of the histogram kernels: one red.shared per (cell or regrouped vertex, direction).
+SMEM_ATOMS_PER_CLK_SM = 16.0
+
+
+def alu_peak(sm_mhz):
+    """Peak shared-atomic updates per second: 148 SMs x 16 lane-ops/clk x the max SM clock."""
+    return 148 * SMEM_ATOMS_PER_CLK_SM * sm_mhz * 1e6
+
+
 def load_traffic(key):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -122,7 +133,8 @@ def workload(cfg: str, rank: int):
         out_dtype = "int32" if 255 * ncells < 2 ** 31 else "int64"
         osz = 4 if out_dtype == "int32" else 8
         return dict(kind="images", name=spec["name"], img=img, dirs=dirs, T=spec["T"], B=B, out_dtype=out_dtype,
-                    units=B, updates=B * ncells * spec["D"], alg_bytes=B * nv + B * spec["D"] * spec["T"] * osz,
+                    units=B, updates=B * ncells * spec["D"], atomics=B * nv * spec["D"],
+                    alg_bytes=B * nv + B * spec["D"] * spec["T"] * osz,
                     unit="complexes/s", desc=f"{B}x{'x'.join(map(str, dims))} u8 images, D={spec['D']}, T={spec['T']}, {out_dtype} out")
     if cfg in ("3", "4", "ecfx"):
         c = 3 if cfg in ("3", "ecfx") else 4
@@ -139,6 +151,7 @@ def workload(cfg: str, rank: int):
                         desc=f"ECF of the cfg4 torus mesh ({cx.k0} V, {ncells} cells), m=1 filter, T={T}")
         D = dirs.shape[0]
         return dict(kind="complex", name=d["name"], cx=cx, dirs=dirs, T=T, units=1, updates=ncells * D,
+                    atomics=ncells * D,
                     alg_bytes=cx.coords.nbytes + idx_bytes + w_bytes + D * T * 8, unit="complexes/s",
                     desc=f"explicit complex {cx.k0} V / {ncells} cells, n={cx.n}, D={D}, T={T}, "
                          f"{'f32' if cx.is_float else 'i32'} weights")
@@ -157,6 +170,7 @@ def run_ours(args, rank, world, local_rank):
     if args.D and "dirs" in wl and wl["kind"] == "complex":
         wl["dirs"] = np.ascontiguousarray(wl["dirs"][: args.D])
         wl["updates"] = wl["updates"] // synth.CONFIGS[int(args.config)]["D"] * args.D
+        wl["atomics"] = wl["updates"]
         wl["alg_bytes"] += (args.D - synth.CONFIGS[int(args.config)]["D"]) * wl["T"] * 8
         wl["name"] += f"_D{args.D}"
     stream = torch.cuda.current_stream(dev)
@@ -230,10 +244,34 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = total_ms / K
     value = world * wl["units"] * K / (total_ms / 1e3)
     peak, peak_src = load_peaks()
-    achieved = wl["alg_bytes"] / (main_ms / 1e3) / 1e9
-    kname = {"images": "k_sweep2d" if args.config in ("0", "1") else "k_grid_hist",
-             "complex": "k_complex", "ecf": "k_complex(ECF)"}[wl["kind"]]
-    traffic = load_traffic(f"cfg{args.config}")
+    per_call_launches = tl / max(K, 1)  # timed (dominant-kernel) launches per step
+    D = wl["dirs"].shape[0] if "dirs" in wl else 1
+    if wl["kind"] == "images" and args.config in ("0", "1"):
+        kname, bound = "k_sweep2d", "hbm"
+    elif wl["kind"] == "images":
+        kname, bound = "k_grid_hist", "alu"
+    elif wl["kind"] == "ecf" or D <= 8:
+        kname, bound = "k_stream", "hbm"
+    else:
+        kname, bound = "k_cells_vb", "alu"
+    if bound == "hbm":
+        achieved = wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9
+        roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src,
+                "alg_bytes_per_launch": wl["alg_bytes"] / per_call_launches}
+    else:
+        # algorithmic work = shared-memory histogram updates: (cell, direction) pairs for
+        # explicit complexes, regrouped (vertex, direction) pairs for voxel grids
+        work = wl["atomics"] / per_call_launches
+        apeak = alu_peak(float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0))
+                         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0)
+        achieved = work / (main_ms / 1e3) / 1e9
+        roof = {"kernel": kname, "bound": "alu", "achieved": achieved, "peak": apeak / 1e9, "unit": "Gupdates/s",
+                "frac": achieved * 1e9 / apeak,
+                "peak_source": "148 SMs x 16 shared int32 atomic lane-ops/clk (tools/microbench/smem_ubench.cu) x sm_max_mhz",
+                "work_per_launch": work,
+                "hbm_achieved_gbs": wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9}
+    traffic = load_traffic(f"cfg{args.config}" + (f"_D{args.D}" if args.D else ""))
     res = {
         "metric": METRIC,
         "value": value,
@@ -252,10 +290,8 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"batch-sharded dp{world}" if wl["kind"] == "images" else f"replicas x{world}"},
         "updates_per_s": world * wl["updates"] * K / (total_ms / 1e3),
         "hbm_gbs": world * wl["alg_bytes"] * K / (total_ms / 1e3) / 1e9,
-        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "alg_bytes_per_launch": wl["alg_bytes"], "kernel_ms": main_ms,
-                     "kernel_share_of_step": main_ms / ms_per_step},
+        "roofline": dict(roof, traffic=traffic, kernel_ms=main_ms, launches_per_step=per_call_launches,
+                         kernel_share_of_step=main_ms * per_call_launches / ms_per_step),
         "gpu_launches": int(launches),
         "repairs_binary64": int(repairs),
         "clocks": sampler.summary(),
