@@ -210,7 +210,50 @@ __global__ void __launch_bounds__(kVbWarps * 32, 1) k_cells_vb(Segs segs, int64_
     limit = 32768;
   }
   int64_t since = 0;
+  const int nseg = segs.nseg;
   __syncthreads();
+  // Per-warp cursor over (step, segment, batch): the next batch's ids and weights are
+  // loaded into registers (pv, pw) while the current one is processed, so the HBM
+  // latency of the streamed cell lists is off the critical path.
+  struct Cur {
+    int step, sg, u;
+  };
+  auto seek = [&](int step, int sg, int u) -> Cur {  // first batch at or after (step, sg, u)
+    while (step < nstep) {
+      while (sg < nseg) {
+        if (u < __ldg(bat + sg * nstep + step)) return Cur{step, sg, u};
+        ++sg;
+        u = (int)gw;
+      }
+      ++step;
+      sg = 0;
+    }
+    return Cur{nstep, 0, 0};
+  };
+  constexpr int PF = 5;  // prefetched ids per lane: batches of arity <= 5
+  int pv[PF];
+  Acc pw = (Acc)0;
+  int64_t pb0 = 0;
+  int pnb = 0;
+  auto fetch = [&](const Cur& c) {
+    const Seg& S = ssegs[c.sg];
+    const int ar = S.arity;
+    const int bs = (kVbBatch * 8) / ar > kVbBatch ? kVbBatch : (kVbBatch * 8) / ar;
+    const int64_t c0 = __ldg(bnd + c.sg * (int64_t)(nstep + 1) + c.step);
+    const int64_t c1 = __ldg(bnd + c.sg * (int64_t)(nstep + 1) + c.step + 1);
+    pb0 = c0 + (int64_t)c.u * bs;
+    pnb = (c1 - pb0) < bs ? (int)(c1 - pb0) : bs;
+    if (ar <= PF) {
+#pragma unroll
+      for (int k = 0; k < PF; ++k) {
+        const int t = lane + 32 * k;
+        pv[k] = t < pnb * ar ? (S.verts ? __ldg(S.verts + pb0 * ar + t) : (int)(pb0 + t)) : 0;
+      }
+    }
+    pw = lane < pnb ? cell_weight<FLOATW, Acc>(S, pb0 + lane) : (Acc)0;
+  };
+  Cur nxt = seek(0, 0, (int)gw);
+  if (nxt.step < nstep) fetch(nxt);
   for (int step = 0; step < nstep; ++step) {
     const int64_t cta_cells = __ldg(bound + step);  // k_step_info: cells one CTA may take this step
     // a step alone could overflow the int32 partials: add straight into int64 instead
@@ -224,48 +267,58 @@ __global__ void __launch_bounds__(kVbWarps * 32, 1) k_cells_vb(Segs segs, int64_
       since = 0;
     }
     since += cta_cells;
-    for (int sg = 0; sg < segs.nseg; ++sg) {
-      const Seg& S = ssegs[sg];
+    while (nxt.step == step) {
+      const Cur cur = nxt;
+      const Seg& S = ssegs[cur.sg];
       const int ar = S.arity;
-      const int bs = (kVbBatch * 8) / ar > kVbBatch ? kVbBatch : (kVbBatch * 8) / ar;
-      const int U = __ldg(bat + sg * nstep + step);
-      if ((int)gw >= U) continue;
-      const int64_t c0 = __ldg(bnd + sg * (int64_t)(nstep + 1) + step);
-      const int64_t c1 = __ldg(bnd + sg * (int64_t)(nstep + 1) + step + 1);
-      for (int u = (int)gw; u < U; u += (int)W) {
-        const int64_t b0 = c0 + (int64_t)u * bs;
-        const int nb = (c1 - b0) < bs ? (int)(c1 - b0) : bs;
-        unsigned badcells = 0;
+      const int64_t b0 = pb0;
+      const int nb = pnb;
+      Acc wl = pw;
+      // stage the current batch's ids (validated) from the prefetch registers
+      unsigned badcells = 0;
+      if (ar <= PF) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+          const int t = lane + 32 * k;
+          if (t < nb * ar) {
+            int v = pv[k];
+            if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
+            ids[t] = v;
+          }
+        }
+      } else {
         for (int t = lane; t < nb * ar; t += 32) {
           int v = S.verts ? __ldg(S.verts + b0 * ar + t) : (int)(b0 + t);
           if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
           ids[t] = v;
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) badcells |= __shfl_xor_sync(0xffffffffu, badcells, o);
-        Acc wl = (Acc)0;
-        if (lane < nb && !((badcells >> lane) & 1u)) wl = cell_weight<FLOATW, Acc>(S, b0 + lane);
-        if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
-        __syncwarp();
-        if (!FLOATW && drow) {
-          switch (ar) {
-            case 1: vb_batch<1, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            case 2: vb_batch<2, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            case 3: vb_batch<3, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            default: vb_batch<0, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
-          }
-        } else {
-          switch (ar) {
-            case 1: vb_batch<1, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            case 2: vb_batch<2, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            case 3: vb_batch<3, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            case 4: vb_batch<4, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            case 5: vb_batch<5, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-            default: vb_batch<0, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
-          }
-        }
-        __syncwarp();
       }
+      // issue the next batch's loads now; they land while this batch is processed
+      nxt = seek(cur.step, cur.sg, cur.u + (int)W);
+      if (nxt.step < nstep) fetch(nxt);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) badcells |= __shfl_xor_sync(0xffffffffu, badcells, o);
+      if ((badcells >> lane) & 1u) wl = (Acc)0;
+      if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
+      __syncwarp();
+      if (!FLOATW && drow) {
+        switch (ar) {
+          case 1: vb_batch<1, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 2: vb_batch<2, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 3: vb_batch<3, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          default: vb_batch<0, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
+        }
+      } else {
+        switch (ar) {
+          case 1: vb_batch<1, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 2: vb_batch<2, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 3: vb_batch<3, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 4: vb_batch<4, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 5: vb_batch<5, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
+          default: vb_batch<0, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
+        }
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
