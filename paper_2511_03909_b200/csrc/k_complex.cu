@@ -373,8 +373,11 @@ wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const
     return launch_cells(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp, wmax, diff, st,
                         num_sms);
   }
-  if (vb_supported(T) && !getenv("WECT_DISABLE_VB"))  // vertex bins once per tile, cells from packed rows
-    return launch_complex_vb(n, floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);
+  if (vb_supported(T) && !getenv("WECT_DISABLE_VB")) {  // vertex bins once per tile, cells from packed rows
+    const wect_status s = launch_complex_vb(n, floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st,
+                                            num_sms);
+    if (s != WECT_ENOTSUP) return s;
+  }
   switch (n) {
 #define WECT_CASE(NN) \
   case NN: return launch_complex_n<NN>(floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st, num_sms);

@@ -98,58 +98,63 @@ __device__ __forceinline__ void red_shared(uint32_t addr, int w) {
   asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
 }
 
-// One batch of nb <= kVbBatch cells of arity AR (0: runtime `arr`) whose ids are staged
-// in `ids` and whose signed weights sit in lane (cell) order in wl: four cells at a time,
-// all their 4*AR row loads issued before the packed max and the adds.  vbl = vb + lane
-// (the lane's column of the VB rows); hsa = shared address of hist + lane (int path) and
-// hl the same as a pointer (float path).  DIRECT (integer weights too large for int32
-// partials over one step): add straight into the int64 difference rows drow[0..T) and
-// drow[T..2T) of the lane's two directions (aa / ab: the direction exists).
-template <int AR, bool FLOATW, bool DIRECT, typename Acc>
-__device__ __forceinline__ void vb_batch(const int* ids, int nb, Acc wl, const uint32_t* __restrict__ vbl,
-                                         uint32_t hsa, Acc* hl, unsigned long long* drow, int T, bool aa, bool ab,
-                                         int arr = AR) {
-  const int ar = AR > 0 ? AR : arr;
-  constexpr int RA = AR > 0 ? AR : 1;
-  for (int j = 0; j < nb; j += 4) {
-    uint32_t m2[4];
-    if (AR > 0) {
-      uint32_t x[4][RA];
+// Record stride (ints) of a staged cell: its AR ids then its signed weight, padded to a
+// power of two so that one LDS.64 / LDS.128 (two for 4 <= AR <= 7) broadcasts a cell.
+__host__ __device__ constexpr int rec_stride(int ar) { return ar + 1 <= 2 ? 2 : (ar + 1 <= 4 ? 4 : 8); }
+
+template <int RS>
+__device__ __forceinline__ void load_rec(const int* r, int* out) {
+  if constexpr (RS == 2) {
+    const int2 q = *(const int2*)r;
+    out[0] = q.x; out[1] = q.y;
+  } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int t = 0; t < RA; ++t) x[u][t] = (j + u < nb) ? __ldg(vbl + (int64_t)ids[(j + u) * RA + t] * 32) : 0u;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        m2[u] = x[u][0];
-#pragma unroll
-        for (int t = 1; t < RA; ++t) m2[u] = __vmaxu2(m2[u], x[u][t]);
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        m2[u] = 0;
-        if (j + u < nb)
-          for (int t = 0; t < ar; ++t) m2[u] = __vmaxu2(m2[u], __ldg(vbl + (int64_t)ids[(j + u) * ar + t] * 32));
-      }
+    for (int i = 0; i < RS; i += 4) {
+      const int4 q = *(const int4*)(r + i);
+      out[i] = q.x; out[i + 1] = q.y; out[i + 2] = q.z; out[i + 3] = q.w;
     }
+  }
+}
+
+// One batch of nb <= kVbBatch cells of arity AR staged as records in `rec` (ids, then
+// the signed weight; dead or invalid cells carry weight 0 and ids 0): four cells at a
+// time, all their 4*AR row loads issued before the packed max and the adds.
+// vbl = vb + lane (the lane's column of the VB rows); hsa = shared address of hist + lane
+// (int path), hl the same as a pointer (float path).  DIRECT (integer weights too large
+// for int32 partials over one step): add straight into the int64 difference rows
+// drow[0..T) and drow[T..2T) of the lane's two directions (aa / ab: the direction exists).
+template <int AR, bool FLOATW, bool DIRECT, typename Acc>
+__device__ __forceinline__ void vb_batch(const int* rec, int nb, const uint32_t* __restrict__ vbl, uint32_t hsa,
+                                         Acc* hl, unsigned long long* drow, int T, bool aa, bool ab) {
+  constexpr int RS = rec_stride(AR);
+  for (int j = 0; j < nb; j += 4) {
+    int r[4][RS];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) load_rec<RS>(rec + (j + u) * RS, r[u]);  // records past nb are zero
+    uint32_t x[4][AR];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int t = 0; t < AR; ++t) x[u][t] = __ldg(vbl + (int64_t)r[u][t] * 32);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const Acc w = __shfl_sync(0xffffffffu, wl, (j + u) & 31);  // 0 past nb
-      const uint32_t lo = m2[u] & 0xFFFFu, hi = m2[u] >> 16;
+      uint32_t m2 = x[u][0];
+#pragma unroll
+      for (int t = 1; t < AR; ++t) m2 = __vmaxu2(m2, x[u][t]);
+      const uint32_t lo = m2 & 0xFFFFu, hi = m2 >> 16;
+      const int wi = r[u][AR];
       if constexpr (DIRECT) {
-        if (j + u < nb && w != (Acc)0) {
-          if (aa) atomicAdd(drow + lo, (unsigned long long)(long long)w);
-          if (ab) atomicAdd(drow + T + hi, (unsigned long long)(long long)w);
+        if (wi != 0) {
+          if (aa) atomicAdd(drow + lo, (unsigned long long)(long long)wi);
+          if (ab) atomicAdd(drow + T + hi, (unsigned long long)(long long)wi);
         }
       } else if constexpr (FLOATW) {
-        if (j + u < nb) {
-          hist_add(hl + lo * 64, w);
-          hist_add(hl + hi * 64 + 32, w);
-        }
-      } else {  // cells past nb carry w = 0 and a harmless bin 0
-        red_shared(hsa + lo * 256u, (int)w);
-        red_shared(hsa + hi * 256u + 128u, (int)w);
+        const float w = __int_as_float(wi);
+        hist_add(hl + lo * 64, w);
+        hist_add(hl + hi * 64 + 32, w);
+      } else {
+        red_shared(hsa + lo * 256u, wi);
+        red_shared(hsa + hi * 256u + 128u, wi);
       }
     }
   }
@@ -230,27 +235,22 @@ __global__ void __launch_bounds__(kVbWarps * 32, 1) k_cells_vb(Segs segs, int64_
     }
     return Cur{nstep, 0, 0};
   };
-  constexpr int PF = 5;  // prefetched ids per lane: batches of arity <= 5
+  constexpr int PF = 7;  // lane = cell of the batch: its <= 7 ids are prefetched
   int pv[PF];
   Acc pw = (Acc)0;
-  int64_t pb0 = 0;
   int pnb = 0;
   auto fetch = [&](const Cur& c) {
     const Seg& S = ssegs[c.sg];
     const int ar = S.arity;
-    const int bs = (kVbBatch * 8) / ar > kVbBatch ? kVbBatch : (kVbBatch * 8) / ar;
     const int64_t c0 = __ldg(bnd + c.sg * (int64_t)(nstep + 1) + c.step);
     const int64_t c1 = __ldg(bnd + c.sg * (int64_t)(nstep + 1) + c.step + 1);
-    pb0 = c0 + (int64_t)c.u * bs;
-    pnb = (c1 - pb0) < bs ? (int)(c1 - pb0) : bs;
-    if (ar <= PF) {
+    const int64_t b0 = c0 + (int64_t)c.u * kVbBatch;
+    pnb = (c1 - b0) < kVbBatch ? (int)(c1 - b0) : kVbBatch;
+    const bool live = lane < pnb;
+    const int64_t b = b0 + lane;
 #pragma unroll
-      for (int k = 0; k < PF; ++k) {
-        const int t = lane + 32 * k;
-        pv[k] = t < pnb * ar ? (S.verts ? __ldg(S.verts + pb0 * ar + t) : (int)(pb0 + t)) : 0;
-      }
-    }
-    pw = lane < pnb ? cell_weight<FLOATW, Acc>(S, pb0 + lane) : (Acc)0;
+    for (int t = 0; t < PF; ++t) pv[t] = (live && t < ar) ? (S.verts ? __ldg(S.verts + b * ar + t) : (int)b) : 0;
+    pw = live ? cell_weight<FLOATW, Acc>(S, b) : (Acc)0;
   };
   Cur nxt = seek(0, 0, (int)gw);
   if (nxt.step < nstep) fetch(nxt);
@@ -269,53 +269,44 @@ __global__ void __launch_bounds__(kVbWarps * 32, 1) k_cells_vb(Segs segs, int64_
     since += cta_cells;
     while (nxt.step == step) {
       const Cur cur = nxt;
-      const Seg& S = ssegs[cur.sg];
-      const int ar = S.arity;
-      const int64_t b0 = pb0;
+      const int ar = ssegs[cur.sg].arity;
       const int nb = pnb;
-      Acc wl = pw;
-      // stage the current batch's ids (validated) from the prefetch registers
-      unsigned badcells = 0;
-      if (ar <= PF) {
+      const int rs = rec_stride(ar);
+      // stage this lane's cell as a record: ids (validated) and signed weight
+      bool bad = false;
 #pragma unroll
-        for (int k = 0; k < PF; ++k) {
-          const int t = lane + 32 * k;
-          if (t < nb * ar) {
-            int v = pv[k];
-            if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
-            ids[t] = v;
-          }
-        }
-      } else {
-        for (int t = lane; t < nb * ar; t += 32) {
-          int v = S.verts ? __ldg(S.verts + b0 * ar + t) : (int)(b0 + t);
-          if ((uint64_t)(int64_t)v >= (uint64_t)k0) { badcells |= 1u << (t / ar); v = 0; }
-          ids[t] = v;
-        }
+      for (int t = 0; t < PF; ++t) bad |= t < ar && (uint64_t)(int64_t)pv[t] >= (uint64_t)k0;
+      {
+        int* r = ids + lane * rs;
+        const int wbits = FLOATW ? __float_as_int((float)pw) : (int)pw;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t < rs) r[t] = bad ? 0 : (t < ar ? pv[t] : (t == ar ? wbits : 0));
       }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&g_err_word, 1u);
       // issue the next batch's loads now; they land while this batch is processed
       nxt = seek(cur.step, cur.sg, cur.u + (int)W);
       if (nxt.step < nstep) fetch(nxt);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) badcells |= __shfl_xor_sync(0xffffffffu, badcells, o);
-      if ((badcells >> lane) & 1u) wl = (Acc)0;
-      if (badcells && lane == 0) atomicOr(&g_err_word, 1u);
       __syncwarp();
       if (!FLOATW && drow) {
         switch (ar) {
-          case 1: vb_batch<1, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          case 2: vb_batch<2, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          case 3: vb_batch<3, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          default: vb_batch<0, FLOATW, true>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
+          case 1: vb_batch<1, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 2: vb_batch<2, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 3: vb_batch<3, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 4: vb_batch<4, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 5: vb_batch<5, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 6: vb_batch<6, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          default: vb_batch<7, FLOATW, true>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
         }
       } else {
         switch (ar) {
-          case 1: vb_batch<1, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          case 2: vb_batch<2, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          case 3: vb_batch<3, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          case 4: vb_batch<4, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          case 5: vb_batch<5, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab); break;
-          default: vb_batch<0, FLOATW, false>(ids, nb, wl, vbl, hsa, hl, drow, T, aa, ab, ar); break;
+          case 1: vb_batch<1, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 2: vb_batch<2, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 3: vb_batch<3, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 4: vb_batch<4, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 5: vb_batch<5, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          case 6: vb_batch<6, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
+          default: vb_batch<7, FLOATW, false>(ids, nb, vbl, hsa, hl, drow, T, aa, ab); break;
         }
       }
       __syncwarp();
@@ -449,6 +440,8 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
                                int d_begin, int Dc, int T, const GridParams* gp, const unsigned int* wmax, void* diff,
                                cudaStream_t st, int num_sms) {
   Segs segs = segs_in;
+  for (int i = 0; i < segs.nseg; ++i)
+    if (segs.s[i].arity > 7) return WECT_ENOTSUP;  // records hold <= 7 ids: k_complex takes it
   uint32_t* vb = nullptr;
   WECT_CUDA_TRY(cudaMallocAsync((void**)&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t), st));
   const size_t smem = (size_t)T * 64 * 4 + (size_t)kVbWarps * kVbBatch * 8 * sizeof(int);

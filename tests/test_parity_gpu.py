@@ -433,3 +433,12 @@ def test_stream_kernel_float_arity5_vs_O2():
     dirs = synth.directions_sphere(5, 4, 3)
     T = 200
     assert_float_close(gpu_wect_complex(cx, dirs, T), oracle.wect_complex(cx, dirs, T), abs_cumsum(cx, dirs, T))
+
+
+def test_high_arity_cells_take_the_generic_kernel():
+    """Arity 8 (7-simplices) at D > 8: the vertex-bin path declines (records hold <= 7
+    ids) and k_complex computes it; arity 6-7 stay on the vertex-bin path."""
+    for kmax, seed in ((7, 91), (6, 92), (5, 93)):
+        cx = synth.random_small_complex(seed, n=3, nverts=60, ntop=12, kmax=kmax)
+        dirs = synth.directions_sphere(40, 3, seed)
+        assert (gpu_wect_complex(cx, dirs, 97) == oracle.wect_complex(cx, dirs, 97)).all()
