@@ -466,6 +466,9 @@ __device__ __noinline__ int grid_repair(float cx, float cy, float cz, float s0, 
 }
 
 // predicated shared-memory add (no branch, no reconvergence barrier)
+__device__ __forceinline__ void red_shared_add(uint32_t addr, int w) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
+}
 __device__ __forceinline__ void red_shared_nz(uint32_t addr, int w) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, 0;\n\t@p red.shared.add.s32 [%0], %1;\n\t}" ::"r"(addr), "r"(w));
 }
@@ -503,7 +506,6 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
   const float A = g.A, Bc = g.B, tau = g.fp32_only ? -1.f : g.tau;
   const float a0 = A * s[0] / (float)S;
   const float c0 = (float)((double)(L[0] - 1) / 2.0);
-  const bool clampit = g.lo != -g.M || g.hi != g.M || g.degenerate;
   const int Tm1 = T - 1;
   const uint32_t hlane = (uint32_t)__cvta_generic_to_shared(hist) + 4u * lane;
   const uint32_t* segw = (const uint32_t*)(seg + o * kSegStride);  // this lane's octant row, 2 voxels per word
@@ -537,21 +539,39 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
           seg[oo * kSegStride + k] = cwb[oo * nv + src0 + k];
         }
       }
-      if (nx & 1) seg[o * kSegStride + nx] = 0;  // pad the odd tail voxel (same value by all lanes of o)
+      // zero-pad every octant row to a multiple of 8 voxels (the loop below takes 8 at a time)
+      const int nx8 = (nx + 7) & ~7;
+      for (int t = lane; t < NO * (nx8 - nx); t += 32) {
+        const int oo = t / (nx8 - nx);
+        seg[oo * kSegStride + nx + (t - oo * (nx8 - nx))] = 0;
+      }
       __syncwarp();
-      float xf = (float)x0;
-      for (int xi = 0; xi < nx; xi += 2) {
-        const uint32_t pair = segw[xi >> 1] & amask;
+      // 8 voxels per step: one 16-byte load of this lane's octant row, eight fp32 bins
+      // (branch-free clamp), one guard test for the group, eight red.shared adds
+      for (int xi = 0; xi < nx; xi += 8) {
+        const uint4 q = *(const uint4*)(segw + (xi >> 1));
+        const uint32_t wd[4] = {q.x & amask, q.y & amask, q.z & amask, q.w & amask};
+        const float xf = (float)(x0 + xi);
+        int bin[8];
+        float dist[8], dmin = 2.f;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int w = h == 0 ? (int)(int16_t)(pair & 0xFFFFu) : (int)pair >> 16;
-          const float u = fmaf(xf, a0, U0);
-          xf += 1.f;
-          int bin = __float2int_ru(u);
-          if (__builtin_expect(fabsf(u - rintf(u)) < tau, 0))
-            bin = grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
-          else if (clampit) bin = bin < 0 ? 0 : (bin > Tm1 ? Tm1 : bin);
-          red_shared_nz(hlane + 128u * (uint32_t)bin, w);
+        for (int h = 0; h < 8; ++h) {
+          const float u = fmaf(xf + (float)h, a0, U0);  // x0 + xi + h is exact in fp32
+          bin[h] = max(0, min(__float2int_ru(u), Tm1));
+          dist[h] = fabsf(u - rintf(u));
+          dmin = fminf(dmin, dist[h]);
+        }
+        if (__builtin_expect(dmin < tau, 0)) {  // some voxel of the group sits near a bin edge
+          const int nvalid = nx - xi;  // padding voxels need no repair
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            if (dist[h] < tau && h < nvalid)
+              bin[h] = grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int w = (h & 1) ? (int)wd[h >> 1] >> 16 : (int)(int16_t)(wd[h >> 1] & 0xFFFFu);
+          red_shared_add(hlane + 128u * (uint32_t)bin[h], w);
         }
       }
       __syncwarp();
