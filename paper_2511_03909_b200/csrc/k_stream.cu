@@ -112,6 +112,7 @@ struct StreamCtx {
   const float* coords;  // MODE 1
   const float* sdir;    // MODE 1: [np][N] in shared memory
   int np, T, rl, rmask, row0;
+  float tau;  // near-edge guard; -1 with WECT_FP32_ONLY (never fires)
   bool direct;  // int weights too large for int32 partials: add straight into the int64 table
   uint32_t k0c;
   void* diff;
@@ -138,23 +139,22 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
       for (int k = 0; k < KG; ++k)
 #pragma unroll
         for (int t = 0; t < AR; ++t) h[k][t] = __ldg(fp + (uint32_t)v[k][t] * (uint32_t)c.m);  // k0*m < 2^32
-      float hm[KG];
+      float hm[KG], dist[KG], dmin = 2.f;
       int bin[KG];
-      unsigned near = 0;
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         hm[k] = h[k][0];
 #pragma unroll
         for (int t = 1; t < AR; ++t) hm[k] = fmaxf(hm[k], h[k][t]);
         const float uu = fmaf(hm[k], c.g.A, c.g.B);
-        const int b = __float2int_ru(uu);
-        bin[k] = max(0, min(b, c.T - 1));
-        near |= (fabsf(uu - rintf(uu)) < c.g.tau ? 1u : 0u) << k;
+        bin[k] = max(0, min(__float2int_ru(uu), c.T - 1));
+        dist[k] = fabsf(uu - rintf(uu));
+        dmin = fminf(dmin, dist[k]);
       }
-      if (__builtin_expect(near != 0 && !c.g.fp32_only, 0)) {
+      if (__builtin_expect(dmin < c.tau, 0)) {  // some cell of the group sits near a bin edge
 #pragma unroll
         for (int k = 0; k < KG; ++k)
-          if ((near >> k) & 1u) bin[k] = stream_ecf_repair(hm[k], c.gp);
+          if (dist[k] < c.tau) bin[k] = stream_ecf_repair(hm[k], c.gp);
       }
       if (!FLOATW && c.direct) {
 #pragma unroll
@@ -181,7 +181,7 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
 #pragma unroll
       for (int i = 0; i < N; ++i) sv[i] = s[i];
       int bin[KG];
-      unsigned near = 0;
+      float dist[KG], dmin = 2.f;
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         float hmax = -FLT_MAX;
@@ -193,14 +193,14 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
           hmax = fmaxf(hmax, h);
         }
         const float uu = fmaf(hmax, c.g.A, c.g.B);
-        const int b = __float2int_ru(uu);
-        bin[k] = max(0, min(b, c.T - 1));
-        near |= (fabsf(uu - rintf(uu)) < c.g.tau ? 1u : 0u) << k;
+        bin[k] = max(0, min(__float2int_ru(uu), c.T - 1));
+        dist[k] = fabsf(uu - rintf(uu));
+        dmin = fminf(dmin, dist[k]);
       }
-      if (__builtin_expect(near != 0 && !c.g.fp32_only, 0)) {
+      if (__builtin_expect(dmin < c.tau, 0)) {
 #pragma unroll
         for (int k = 0; k < KG; ++k)
-          if ((near >> k) & 1u) {
+          if (dist[k] < c.tau) {
             CellIds<AR> ids;
 #pragma unroll
             for (int t = 0; t < AR; ++t) ids.v[t] = v[k][t];
@@ -222,7 +222,9 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
 // and weights are all in the stage (the producer stores a segment's last <= 3 ids /
 // weights itself, which a 16-byte bulk copy cannot carry).  Releases the stage (one
 // arrive per warp) as soon as the ids are in registers.
-template <int MODE, int N, bool FLOATW, int AR>
+// FAST: a full unit of a segment with index lists and weights (the common case): no
+// liveness or null-pointer tests, and invalid ids are handled out of line.
+template <int MODE, int N, bool FLOATW, int AR, bool FAST>
 __device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c, const Seg S, int64_t b0, int cells,
                                             const int* sid, const void* sw, uint64_t* empty, int ctid, int lane) {
   using Acc = typename StreamCtx<MODE, N, FLOATW>::Acc;
@@ -234,7 +236,7 @@ __device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c,
 #pragma unroll
   for (int k = 0; k < CPT; ++k) {
     const int cl = ctid + k * 32 * kStreamConsumers;  // strided: conflict-free shared loads
-    if (S.verts) {
+    if (FAST || S.verts) {
       const int* p = sid + cl * AR;
       if constexpr (AR == 4) {
         const int4 q = *(const int4*)p;
@@ -250,11 +252,21 @@ __device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c,
 #pragma unroll
       for (int t = 0; t < AR; ++t) v[k][t] = (int)(b0 + cl);
     }
-    const Acc wk = S.weights ? ((const Acc*)sw)[cl] : (Acc)1;
+    const Acc wk = (FAST || S.weights) ? ((const Acc*)sw)[cl] : (Acc)1;
     w[k] = S.sign < 0 ? -wk : wk;
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);  // stage free for the producer
+  bool anybad = !FAST;
+  if (FAST) {
+    bool oob = false;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k)
+#pragma unroll
+      for (int t = 0; t < AR; ++t) oob |= (uint32_t)v[k][t] >= c.k0c;
+    anybad = oob;
+  }
+  if (anybad)
 #pragma unroll
   for (int k = 0; k < CPT; ++k) {
     const int cl = ctid + k * 32 * kStreamConsumers;
@@ -383,6 +395,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   c.rmask = R - 1;
   c.k0c = k0 > 0x80000000ll ? 0x80000000u : (uint32_t)k0;
   c.g = g;
+  c.tau = g.fp32_only ? -1.f : g.tau;
   c.gp = gp;
   c.hist = hist;
   c.row0 = tile * kStreamTile;
@@ -417,7 +430,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     switch (S.arity) {
 #define WECT_AR(A)                                                                                         \
   case A:                                                                                                  \
-    stream_unit<MODE, NS, FLOATW, A>(c, S, b0, cells, sid, swp, &empty[st], tid, lane); \
+    if (cells == stream_unit_cells(A) && S.verts && S.weights)                                             \
+      stream_unit<MODE, NS, FLOATW, A, true>(c, S, b0, cells, sid, swp, &empty[st], tid, lane);            \
+    else                                                                                                   \
+      stream_unit<MODE, NS, FLOATW, A, false>(c, S, b0, cells, sid, swp, &empty[st], tid, lane);           \
     break;
       WECT_AR(1) WECT_AR(2) WECT_AR(3) WECT_AR(4) WECT_AR(5)
 #undef WECT_AR
