@@ -72,6 +72,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
       : "memory");
 }
+// L2 prefetch of [p, p + bytes) (16-byte multiples) through the bulk-copy engine
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // a pointer the compiler cannot re-associate with the 32-bit offsets added to it
 __device__ __forceinline__ const float* opaque(const float* p) {
   const float* q;
@@ -286,6 +291,96 @@ __device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c,
   for (int k0 = 0; k0 < CPT; k0 += KG) stream_group<MODE, N, FLOATW, AR, KG>(c, v + k0, w + k0, lane);
 }
 
+// ---- ECF with one filter per tile (MODE 0, np == 1): software-pipelined over units.
+// ecf_read takes a unit's ids and weights out of its stage, releases the stage and
+// issues the unit's gathers; ecf_finish bins and adds a unit whose gathers were issued
+// one unit earlier, so the L2 latency of the gathers overlaps the previous unit's work.
+template <bool FLOATW, int AR>
+__device__ __forceinline__ void ecf_read(const StreamCtx<0, 1, FLOATW>& c, const Seg& S, int64_t b0, int cells,
+                                         const int* sid, const void* sw, uint64_t* empty, int ctid, int lane,
+                                         float (&h)[stream_unit_cells(AR) / (32 * kStreamConsumers)][AR],
+                                         typename StreamCtx<0, 1, FLOATW>::Acc (&w)[stream_unit_cells(AR) / (32 * kStreamConsumers)]) {
+  using Acc = typename StreamCtx<0, 1, FLOATW>::Acc;
+  constexpr int CPT = stream_unit_cells(AR) / (32 * kStreamConsumers);
+  int v[CPT][AR];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int cl = ctid + k * 32 * kStreamConsumers;
+    if (S.verts) {
+      const int* p = sid + cl * AR;
+      if constexpr (AR == 4) {
+        const int4 q = *(const int4*)p;
+        v[k][0] = q.x; v[k][1] = q.y; v[k][2] = q.z; v[k][3] = q.w;
+      } else if constexpr (AR == 2) {
+        const int2 q = *(const int2*)p;
+        v[k][0] = q.x; v[k][1] = q.y;
+      } else {
+#pragma unroll
+        for (int t = 0; t < AR; ++t) v[k][t] = p[t];
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < AR; ++t) v[k][t] = (int)(b0 + cl);
+    }
+    const Acc wk = S.weights ? ((const Acc*)sw)[cl] : (Acc)1;
+    w[k] = S.sign < 0 ? -wk : wk;
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int cl = ctid + k * 32 * kStreamConsumers;
+    bool oob = false;
+#pragma unroll
+    for (int t = 0; t < AR; ++t) oob |= (uint32_t)v[k][t] >= c.k0c;
+    bad |= cl < cells && oob;
+    if (cl >= cells || oob) {
+      w[k] = (Acc)0;
+#pragma unroll
+      for (int t = 0; t < AR; ++t) v[k][t] = 0;
+    }
+  }
+  if (bad) atomicOr(&g_err_word, 1u);
+  const float* fp = opaque(c.fv);
+#pragma unroll
+  for (int k = 0; k < CPT; ++k)
+#pragma unroll
+    for (int t = 0; t < AR; ++t) h[k][t] = __ldg(fp + (uint32_t)v[k][t] * (uint32_t)c.m);
+}
+
+template <bool FLOATW, int AR>
+__device__ __forceinline__ void ecf_finish(const StreamCtx<0, 1, FLOATW>& c,
+                                           const float (&h)[stream_unit_cells(AR) / (32 * kStreamConsumers)][AR],
+                                           const typename StreamCtx<0, 1, FLOATW>::Acc (&w)[stream_unit_cells(AR) / (32 * kStreamConsumers)],
+                                           int lane) {
+  constexpr int CPT = stream_unit_cells(AR) / (32 * kStreamConsumers);
+  float hm[CPT], dist[CPT], dmin = 2.f;
+  int bin[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    hm[k] = h[k][0];
+#pragma unroll
+    for (int t = 1; t < AR; ++t) hm[k] = fmaxf(hm[k], h[k][t]);
+    const float uu = fmaf(hm[k], c.g.A, c.g.B);
+    bin[k] = max(0, min(__float2int_ru(uu), c.T - 1));
+    dist[k] = fabsf(uu - rintf(uu));
+    dmin = fminf(dmin, dist[k]);
+  }
+  if (__builtin_expect(dmin < c.tau, 0)) {
+#pragma unroll
+    for (int k = 0; k < CPT; ++k)
+      if (dist[k] < c.tau) bin[k] = stream_ecf_repair(hm[k], c.gp);
+  }
+  if (!FLOATW && c.direct) {
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) stream_add_direct(c.diff, (int64_t)c.row0 * c.T + bin[k], (int)w[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) atomicAdd(c.hist + ((bin[k] << c.rl) | (lane & c.rmask)), w[k]);
+  }
+}
+
 template <bool FLOATW, typename Acc>
 __device__ __forceinline__ void stream_flush(Acc* hist, int np, int T, int rl, int row0, int Dc, void* diff,
                                              int ctid) {
@@ -311,7 +406,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     k_stream(Segs segs, StreamUnits su, int64_t k0, const float* __restrict__ fvals, int m,
              const float* __restrict__ coords, const float* __restrict__ dirs, int d_begin, int Dc,
              const GridParams* __restrict__ gp, int rl, const unsigned int* __restrict__ wmax_bits,
-             int64_t float_chunk, void* __restrict__ diff) {
+             int64_t float_chunk, const char* __restrict__ pf, int64_t pf_bytes, void* __restrict__ diff) {
   using Acc = typename std::conditional<FLOATW, float, int>::type;
   constexpr int NS = N > 0 ? N : 1;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -357,6 +452,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 
   if (warp == kStreamConsumers) {  // ---- producer warp
     if (lane == 0) {
+      // warm the L2 with this CTA's share of the gathered array (filter values or
+      // coordinates), so that the first touches of the gathers do not wait on HBM
+      if (pf_bytes > 0) {
+        const int64_t share = ((pf_bytes + G - 1) / G + 15) & ~(int64_t)15;
+        const int64_t a0 = (int64_t)blockIdx.x * share;
+        const int64_t a1 = (a0 + share) < pf_bytes ? (a0 + share) : (pf_bytes & ~(int64_t)15);
+        for (int64_t a = a0; a < a1; a += 32768)
+          bulk_prefetch_l2(pf + a, (unsigned)((a1 - a) < 32768 ? (a1 - a) : 32768));
+      }
       const uint64_t pol = l2_evict_first();
       int sg = 0;
       for (int64_t j = 0; j < my_units; ++j) {
@@ -411,6 +515,68 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   }
   int64_t since = 0;
   int sg = 0;
+  bool small_ar = true;  // the pipelined path keeps two units of gathers in registers: arity <= 3
+  for (int i = 0; i < segs.nseg; ++i) small_ar &= ssegs[i].arity <= 3;
+  if constexpr (MODE == 0) {
+    if (np == 1 && small_ar) {
+      const StreamCtx<0, 1, FLOATW>& c1 = *reinterpret_cast<const StreamCtx<0, 1, FLOATW>*>(&c);
+      int64_t j = 0;
+      while (j < my_units) {
+        int cells;
+        int64_t b0;
+        locate(blockIdx.x + j * G, sg, b0, cells);
+        const Seg S = ssegs[sg];
+        // this CTA's units of segment sg: j in [j, j1)
+        const int64_t uend = sustart[sg + 1];
+        const int64_t j1 = uend > blockIdx.x ? (uend - blockIdx.x + G - 1) / G : 0;
+        const int uc = stream_unit_cells(S.arity);
+        auto unit_cells = [&](int64_t jj) {
+          const int64_t bb = (blockIdx.x + jj * G - sustart[sg]) * uc;
+          return (S.count - bb) < uc ? (int)(S.count - bb) : uc;
+        };
+        auto flush_if = [&](int ncell) {  // uniform across consumer threads
+          if (since + ncell > every_cells) {
+            consumers_sync();
+            stream_flush<FLOATW, Acc>(hist, np, T, rl, tile * kStreamTile, Dc, diff, tid);
+            consumers_sync();
+            since = 0;
+          }
+          since += ncell;
+        };
+        switch (S.arity) {
+#define WECT_ECF_AR(A)                                                                                       \
+  case A: {                                                                                                  \
+    constexpr int CPT = stream_unit_cells(A) / (32 * kStreamConsumers);                                     \
+    float h0[CPT][A], h1[CPT][A];                                                                            \
+    Acc w0[CPT], w1[CPT];                                                                                    \
+    auto rd = [&](int64_t jj, float(&h)[CPT][A], Acc(&w)[CPT]) {                                            \
+      const int st = (int)(jj % kStreamStages);                                                              \
+      const int64_t bb = (blockIdx.x + jj * G - sustart[sg]) * uc;                                          \
+      mbar_wait(&full[st], (unsigned)((jj / kStreamStages) & 1));                                           \
+      ecf_read<FLOATW, A>(c1, S, bb, unit_cells(jj), (const int*)(sidx + st * kStreamIdxBytes),           \
+                          sw + st * kStreamWBytes, &empty[st], tid, lane, h, w);                              \
+    };                                                                                                       \
+    rd(j, h0, w0);                                                                                           \
+    for (; j < j1; j += 2) {                                                                                 \
+      if (j + 1 < j1) rd(j + 1, h1, w1);                                                                     \
+      flush_if(unit_cells(j));                                                                               \
+      ecf_finish<FLOATW, A>(c1, h0, w0, lane);                                                               \
+      if (j + 1 >= j1) { j += 1; break; }                                                                    \
+      if (j + 2 < j1) rd(j + 2, h0, w0);                                                                     \
+      flush_if(unit_cells(j + 1));                                                                           \
+      ecf_finish<FLOATW, A>(c1, h1, w1, lane);                                                               \
+    }                                                                                                        \
+    j = j1;                                                                                                  \
+  } break;
+          WECT_ECF_AR(1) WECT_ECF_AR(2) WECT_ECF_AR(3)
+#undef WECT_ECF_AR
+        }
+      }
+      consumers_sync();
+      stream_flush<FLOATW, Acc>(hist, np, T, rl, tile * kStreamTile, Dc, diff, tid);
+      return;
+    }
+  }
   for (int64_t j = 0; j < my_units; ++j) {
     const int st = (int)(j % kStreamStages);
     int cells;
@@ -453,6 +619,10 @@ static wect_status launch_stream_t(bool floatw, const Segs& segs, const StreamUn
                                    cudaStream_t st, int num_sms) {
   const int tiles = (Dc + kStreamTile - 1) / kStreamTile;
   const int np = Dc < kStreamTile ? Dc : kStreamTile;
+  // the gathered array, prefetched into L2 when it fits comfortably
+  const char* pf = MODE == 0 ? (const char*)fvals : (const char*)coords;
+  int64_t pf_bytes = k0 * (int64_t)(MODE == 0 ? m : N) * 4;
+  if (pf_bytes > ((int64_t)64 << 20) || ((uintptr_t)pf & 15)) pf_bytes = 0;
   const size_t smem = (size_t)kStreamStages * (kStreamIdxBytes + kStreamWBytes) + ((size_t)np * T * 4 << rl);
   int per_tile = num_sms / tiles;
   per_tile = per_tile < 1 ? 1 : per_tile;
@@ -464,12 +634,12 @@ static wect_status launch_stream_t(bool floatw, const Segs& segs, const StreamUn
     auto k = k_stream<MODE, N, true>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, kStreamThreads, smem, st>>>(segs, su, k0, fvals, m, coords, dirs, d_begin, Dc, gp, rl, wmax, 8192,
-                                          diff);
+                                          pf, pf_bytes, diff);
   } else {
     auto k = k_stream<MODE, N, false>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, kStreamThreads, smem, st>>>(segs, su, k0, fvals, m, coords, dirs, d_begin, Dc, gp, rl, wmax, 8192,
-                                          diff);
+                                          pf, pf_bytes, diff);
   }
   count_launch();
   timer.stop();
@@ -477,11 +647,21 @@ static wect_status launch_stream_t(bool floatw, const Segs& segs, const StreamUn
   return WECT_OK;
 }
 
-wect_status launch_stream(int mode, int n, bool floatw, const Segs& segs, int64_t k0, const float* fvals, int m,
+wect_status launch_stream(int mode, int n, bool floatw, const Segs& segs_in, int64_t k0, const float* fvals, int m,
                           const float* coords, const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
                           const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
   if (getenv("WECT_DISABLE_STREAM")) return WECT_ENOTSUP;
   if ((uint64_t)k0 * (uint64_t)(mode == 1 ? m : n) >= ((uint64_t)1 << 32)) return WECT_ENOTSUP;  // 32-bit offsets
+  // process the vertex segment last: by then the cells have pulled the filter values /
+  // coordinates into L2, so its loads hit (the order does not change the sums)
+  Segs segs = segs_in;
+  for (int i = 0; i + 1 < segs.nseg; ++i)
+    if (!segs.s[i].verts) {
+      const Seg v = segs.s[i];
+      for (int j = i; j + 1 < segs.nseg; ++j) segs.s[j] = segs.s[j + 1];
+      segs.s[segs.nseg - 1] = v;
+      break;
+    }
   StreamUnits su;
   su.ustart[0] = 0;
   for (int i = 0; i < segs.nseg; ++i) {
