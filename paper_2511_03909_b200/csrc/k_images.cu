@@ -100,16 +100,15 @@ __global__ void k_grid_params(int ndim, int64_t d0, int64_t d1, int64_t d2, cons
 // sort by bin, and the direction's SWEEP PROGRAM:
 //   off[k]  : packets of four u32 byte offsets (id * 128) into the cw table, k < npk;
 //             each bin's ids are padded to whole packets with the padding row HW
-//             (whose packed value is the bias, i.e. weight 0)
-//   meta[g]  : one byte per packet of group g (4 packets): bit 0 "end of chunk" (fold the
-//              packed sums into the running totals), bits 1..7 emit = number of bins
-//              whose value is the running total after this packet (bin q with z empty
-//              bins after it emits 1 + z; chunk splits of bins with > kMaxRun ids emit 0;
-//              leading empty bins and emits > kMaxEmit ride on all-padding packets).
+//             (packed value 0, i.e. weight 0)
+//   meta[g]  : one byte per packet of group g (4 packets): bit 0 set on every packet that
+//              carries metadata (informational), bits 1..7 emit = number of bins whose
+//              value is the running total after this packet (bin q with z empty bins
+//              after it emits 1 + z; leading empty bins and emits > kMaxEmit ride on
+//              all-padding packets).
 //              Loaded with the packets, so no dependent load sits on the run-end path.
 // Also records the direction's quadrant o = (s_x > 0) | (s_y > 0) << 1 in qlist.
 // ---------------------------------------------------------------------------
-constexpr int kMaxRun = 128;     // ids per chunk: 128 * 510 < 65536, no carry between packed halves
 
 constexpr int kMaxEmit = 127;    // emit field of a packet's metadata byte
 
@@ -162,7 +161,6 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
       while (q2 < T && counts[q2] == 0) ++q2;
       const int npk = (counts[q] + 3) / 4;
       base[q] = pk;
-      for (int k = kMaxRun / 4 - 1; k < npk - 1; k += kMaxRun / 4) meta[pk + k] = 1 << 16;  // chunk split
       int emit = q2 - q;
       int e = emit < kMaxEmit ? emit : kMaxEmit;
       meta[pk + npk - 1] = e | (1 << 16);
@@ -203,7 +201,6 @@ constexpr int kSweepWarps = 16;
 constexpr int kSweepImgs = 64;   // images per CTA group: lane l owns images 2l, 2l+1
 constexpr int kStageBins = 8;    // bins per staged output chunk
 constexpr int kStageStride = 68; // words per staged bin row (68 = 4 mod 32: conflict-free readout)
-constexpr int kBias = 255;       // cw in [-255, 255] -> biased u16 in [0, 510]
 constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -254,19 +251,29 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   return v;
 }
 
+// Signed packed pair: P = S0 + S1 * 2^16 (mod 2^32) with |S0|, |S1| < 2^15 -> (S0, S1).
+__device__ __forceinline__ int2 unpack_s16x2(uint32_t P) {
+  const int s0 = (int)(int16_t)(P & 0xFFFFu);
+  return make_int2(s0, ((int)P - s0) >> 16);
+}
+
 // One warp, one direction, the CTA's 64 images: run the direction's sweep program
-// (packets of 4 cw-row offsets), accumulating packed biased weights and emitting the
-// running (cumulative) sum for every bin.  prg: warp-private smem copy of the program;
-// lane4: shared-window address of this lane's column of the cw table.  Packets are
-// consumed four at a time: all 16 gathers are issued before the (warp-uniform)
-// end-of-chunk checks, so each warp keeps 16 shared loads in flight.
+// (packets of 4 cw-row offsets), accumulating the signed packed weights of images
+// (2l, 2l+1) and emitting the running (cumulative) sum for every bin.  Packets are
+// consumed four at a time (a group): all 16 gathers are issued first and summed into
+// group-local packed partials P[j] (|half| <= 16 * 255, so no carry ever crosses a
+// half); emits unpack P[j] onto the int32 base, and the group's total is folded into
+// the base once per group.
 template <typename OutT>
 __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* __restrict__ prg, int npk, int Lp,
                                                 int* __restrict__ st, OutT* __restrict__ out, int64_t img0, int nimg,
                                                 int Dc, int dl, int T, int lane) {
   const uint4* pk = (const uint4*)prg;
   const uint32_t* metaw = prg + 4 * Lp;
-  int q = 0, tot0 = 0, tot1 = 0;
+  int q = 0, base0 = 0, base1 = 0;
+  const bool fast = sizeof(OutT) == 4 && nimg == kSweepImgs && (T % kStageBins) == 0;
+  OutT* const lp = out + ((img0 + (lane >> 1)) * Dc + dl) * (int64_t)T + 4 * (lane & 1);
+  const int64_t rstride = (int64_t)16 * Dc * T;
   // the program streams from L2: prefetch it into L1 (one 128-byte line per lane)
   if (lane * 8 < npk) asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + lane * 8));
   if (lane * 32 < npk / 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(metaw + lane * 32));
@@ -276,33 +283,50 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
   for (int k = 0; k < npk; k += 4) {
     if ((k & 255) == 252 && lane * 8 + k + 4 < npk)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + k + 4 + lane * 8));
-    uint32_t s[4];
-    s[0] = lds32(lane4 + w0.x) + lds32(lane4 + w0.y) + lds32(lane4 + w0.z) + lds32(lane4 + w0.w);
-    s[1] = lds32(lane4 + w1.x) + lds32(lane4 + w1.y) + lds32(lane4 + w1.z) + lds32(lane4 + w1.w);
-    s[2] = lds32(lane4 + w2.x) + lds32(lane4 + w2.y) + lds32(lane4 + w2.z) + lds32(lane4 + w2.w);
-    s[3] = lds32(lane4 + w3.x) + lds32(lane4 + w3.y) + lds32(lane4 + w3.z) + lds32(lane4 + w3.w);
+    uint32_t P[4];
+    P[0] = lds32(lane4 + w0.x) + lds32(lane4 + w0.y) + lds32(lane4 + w0.z) + lds32(lane4 + w0.w);
+    P[1] = lds32(lane4 + w1.x) + lds32(lane4 + w1.y) + lds32(lane4 + w1.z) + lds32(lane4 + w1.w);
+    P[2] = lds32(lane4 + w2.x) + lds32(lane4 + w2.y) + lds32(lane4 + w2.z) + lds32(lane4 + w2.w);
+    P[3] = lds32(lane4 + w3.x) + lds32(lane4 + w3.y) + lds32(lane4 + w3.z) + lds32(lane4 + w3.w);
+    P[1] += P[0];
+    P[2] += P[1];
+    P[3] += P[2];
     const uint32_t m = mw;
     if (k + 4 < npk) {
       w0 = __ldg(pk + k + 4); w1 = __ldg(pk + k + 5); w2 = __ldg(pk + k + 6); w3 = __ldg(pk + k + 7);
       mw = __ldg(metaw + (k >> 2) + 1);
     }
-    // every packet carries exactly 4 biased loads: fold it straight into the int32 totals
+    if (m & 0xFEFEFEFEu) {  // some packet of the group ends a bin
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      tot0 += (int)(s[j] & 0xFFFFu) - 4 * kBias;
-      tot1 += (int)(s[j] >> 16) - 4 * kBias;
-      const uint32_t mj = (m >> (8 * j)) & 0xFEu;  // emit count (bit 0, the fold, is implicit now)
-      if (mj) {
-        for (int e = (int)(mj >> 1); e > 0; --e) {
-          *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = make_int2(tot0, tot1);
-          if (((++q) & (kStageBins - 1)) == 0) {
-            __syncwarp();
-            sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q - kStageBins, lane);
-            __syncwarp();
+      for (int j = 0; j < 4; ++j) {
+        int e = (int)((m >> (8 * j + 1)) & 0x7Fu);
+        if (e) {
+          const int2 s = unpack_s16x2(P[j]);
+          const int2 v = make_int2(base0 + s.x, base1 + s.y);
+          for (; e > 0; --e) {
+            *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = v;
+            if (((++q) & (kStageBins - 1)) == 0) {
+              __syncwarp();
+              if (fast) {  // full group, int32, whole chunks: unguarded 16-byte stores
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                  const int mm = r * 16 + (lane >> 1), j4 = 4 * (lane & 1);
+                  const int4 x = make_int4(st[(j4 + 0) * kStageStride + mm], st[(j4 + 1) * kStageStride + mm],
+                                           st[(j4 + 2) * kStageStride + mm], st[(j4 + 3) * kStageStride + mm]);
+                  __stcs((int4*)(lp + r * rstride + (q - kStageBins)), x);
+                }
+              } else {
+                sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q - kStageBins, lane);
+              }
+              __syncwarp();
+            }
           }
         }
       }
     }
+    const int2 s = unpack_s16x2(P[3]);
+    base0 += s.x;
+    base1 += s.y;
   }
   if (q & (kStageBins - 1)) {  // the last, partial chunk (T not a multiple of 8)
     __syncwarp();
@@ -327,7 +351,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   const uint32_t lane4 = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
   const int qc0 = qcount[0], qc1 = qcount[1], qc2 = qcount[2], qc3 = qcount[3];
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
-  if (threadIdx.x < 32) cwb[HW * 32 + threadIdx.x] = (uint32_t)kBias | ((uint32_t)kBias << 16);  // padding row
+  if (threadIdx.x < 32) cwb[HW * 32 + threadIdx.x] = 0u;  // padding row: weight 0
 
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t img0 = grp * kSweepImgs;
@@ -359,8 +383,9 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       __syncthreads();  // pix staged / previous quadrant's sweeps done with cwb
       const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
       {
-        // element (v, lane): cw of images 2l, 2l+1 in packed u16x2 arithmetic.
-        // packed = (a + 255 + m_diag) - (m_c + m_r) stays >= 0 per half (cw >= -255).
+        // element (v, lane): cw of images 2l, 2l+1 as the signed packed pair
+        // cw0 + cw1 * 2^16 (mod 2^32): (a + m_diag) - (m_c + m_r) in plain u32 arithmetic
+        // (each operand half <= 510, so the borrow of a negative cw0 lands in cw1's half).
         int v = threadIdx.x >> 5;
         int r = v / W, c = v - r * W;
         const int step_r = kSweepWarps / W, step_c = kSweepWarps - step_r * W;
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
           if (vr) MR = __vmaxu2(A, __byte_perm(*(const uint16_t*)(p0 + dr * W * kPixStride), 0, 0x4140));
           if (vc && vr)
             MD = __vmaxu2(__vmaxu2(MC, MR), __byte_perm(*(const uint16_t*)(p0 + (dr * W + dc) * kPixStride), 0, 0x4140));
-          cwb[v * 32 + lane] = (A + 0x00FF00FFu + MD) - (MC + MR);
+          cwb[v * 32 + lane] = (A + MD) - (MC + MR);
           r += step_r;
           c += step_c;
           if (c >= W) { c -= W; ++r; }
