@@ -9,7 +9,7 @@ wect_images call over the batch = every row of SURVEY.md section 8(a): grid M
 kernel (a0, a4-a7: implicit cells, max rule, signed regrouped accumulation,
 cumsum, 1.97 GB output write).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx|ecfimg|ecfimg1k] [--impl reference]
 
 Multi-GPU (torchrun, one rank per GPU): images are sharded by batch with no data-path
 collective (weak scaling: every rank runs its own 60,000-image shard); times are the
@@ -136,6 +136,20 @@ def workload(cfg: str, rank: int):
                     units=B, updates=B * ncells * spec["D"], atomics=B * nv * spec["D"],
                     alg_bytes=B * nv + B * spec["D"] * spec["T"] * osz,
                     unit="complexes/s", desc=f"{B}x{'x'.join(map(str, dims))} u8 images, D={spec['D']}, T={spec['T']}, {out_dtype} out")
+    if cfg in ("ecfimg", "ecfimg1k"):
+        # image ECF (Remark "which-ecf" P:273-282; T = 256,
+        # one bin per intensity): FMNIST-shaped 60k x 28x28, or 'padded ImageNet' 1000^2
+        B, dims, kind, seed = (60000, (28, 28), "fmnist", synth.S0 + 60) if cfg == "ecfimg" else \
+            (64, (1000, 1000), "uniform", synth.S0 + 61)
+        img = synth.images_u8(B, dims, seed + 7919 * rank, kind)
+        nv = int(np.prod(dims))
+        ncells = int(np.prod([2 * d - 1 for d in dims]))
+        T = 256
+        return dict(kind="ecfimg", name=f"ecf_images_{B}x{'x'.join(map(str, dims))}_T{T}", img=img, T=T, B=B,
+                    out_dtype="int32", units=B, updates=B * ncells, atomics=B * ncells,
+                    alg_bytes=B * nv + B * T * 4, unit="complexes/s",
+                    desc=f"image ECF: {B}x{'x'.join(map(str, dims))} u8 ({kind}), intensity filter, grid [0, 255], "
+                         f"T={T}, int32 out")
     if cfg in ("3", "4", "ecfx"):
         c = 3 if cfg in ("3", "ecfx") else 4
         d = synth.make_config(c)
@@ -175,7 +189,13 @@ def run_ours(args, rank, world, local_rank):
         wl["name"] += f"_D{args.D}"
     stream = torch.cuda.current_stream(dev)
 
-    if wl["kind"] == "images":
+    if wl["kind"] == "ecfimg":
+        img_d = torch.from_numpy(wl["img"]).to(dev)
+        out_d = torch.empty((wl["B"], wl["T"]), dtype=torch.int32, device=dev)
+
+        def step(flags=0):
+            w.ecf_images(img_d, wl["T"], lo=0.0, hi=255.0, out=out_d, flags=flags)
+    elif wl["kind"] == "images":
         img_d = torch.from_numpy(wl["img"]).to(dev)
         dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
         out_d = torch.empty((wl["B"], wl["dirs"].shape[0], wl["T"]),
@@ -246,7 +266,9 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = load_peaks()
     per_call_launches = tl / max(K, 1)  # timed (dominant-kernel) launches per step
     D = wl["dirs"].shape[0] if "dirs" in wl else 1
-    if wl["kind"] == "images" and args.config in ("0", "1"):
+    if wl["kind"] == "ecfimg":
+        kname, bound = ("k_ecf_img_small", "hbm") if args.config == "ecfimg" else ("k_ecf_img_hist", "alu")
+    elif wl["kind"] == "images" and args.config in ("0", "1"):
         kname, bound = "k_sweep2d", "hbm"
     elif wl["kind"] == "images":
         kname, bound = "k_grid_hist", "alu"
@@ -283,11 +305,11 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "int32" if wl.get("out_dtype") == "int32" else ("f64" if wl["kind"] != "images" and wl["cx"].is_float else "int64"),
+        "dtype": "int32" if wl.get("out_dtype") == "int32" else ("f64" if "cx" in wl and wl["cx"].is_float else "int64"),
         "data": "synthetic (seeded; DESIGN.md input recipe)",
         "config": {"workload": wl["name"], "desc": wl["desc"], "per_gpu_units": wl["units"],
                    "l2": f"flushed between timed steps ({flush.numel() >> 20} MiB write, untimed)",
-                   "parallelism": f"batch-sharded dp{world}" if wl["kind"] == "images" else f"replicas x{world}"},
+                   "parallelism": f"batch-sharded dp{world}" if wl["kind"] in ("images", "ecfimg") else f"replicas x{world}"},
         "updates_per_s": world * wl["updates"] * K / (total_ms / 1e3),
         "hbm_gbs": world * wl["alg_bytes"] * K / (total_ms / 1e3) / 1e9,
         "roofline": dict(roof, traffic=traffic, kernel_ms=main_ms, launches_per_step=per_call_launches,
@@ -297,7 +319,27 @@ def run_ours(args, rank, world, local_rank):
         "clocks": sampler.summary(),
     }
     # end to end through the public API with HOST buffers (H2D + compute + D2H every step)
-    if not args.no_e2e and wl["kind"] == "images":
+    if not args.no_e2e and wl["kind"] == "ecfimg":
+        img_h = torch.from_numpy(wl["img"]).pin_memory()
+        out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
+        for _ in range(2):
+            w.ecf_images(img_h, wl["T"], lo=0.0, hi=255.0, out=out_h)
+        ke = max(1, min(5, K))
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            w.ecf_images(img_h, wl["T"], lo=0.0, hi=255.0, out=out_h)
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        res["e2e"] = {"value": world * wl["units"] * ke / e2e_s, "unit": wl["unit"],
+                      "h2d_bytes_per_step": int(img_h.numel()),
+                      "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()), "steps": ke,
+                      "path": "ecf_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"}
+    elif not args.no_e2e and wl["kind"] == "images":
         img_h = torch.from_numpy(wl["img"]).pin_memory()
         dirs_h = torch.from_numpy(wl["dirs"])
         out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
@@ -345,6 +387,19 @@ def cpu_baseline(wl, budget_s=15.0, max_units=None):
     import oracle
 
     cores = oracle.num_threads()
+    if wl["kind"] == "ecfimg":
+        chunk = 200 if wl["img"].shape[1:] == (28, 28) else 1
+        done, t = 0, 0.0
+        limit = wl["B"] if max_units is None else min(max_units, wl["B"])
+        while done < limit and t < budget_s:
+            n = min(chunk, limit - done)
+            t0 = time.perf_counter()
+            oracle.ecf_images(wl["img"][done:done + n], wl["T"], 0.0, 255.0)
+            t += time.perf_counter() - t0
+            done += n
+        return {"value": done / t, "unit": wl["unit"], "cores": cores, "kind": "oracle",
+                "sample": f"O2 (per image, explicit complex) on images [0, {done}) of the {wl['B']}-image workload "
+                          f"({t:.1f} s)"}
     if wl["kind"] == "images" and wl["B"] == 1 and wl["img"][0].size > 1 << 20:
         # one large volume: O2 on 8 sampled directions with the full set's M, scaled to D
         dims = wl["img"].shape[1:]
@@ -396,12 +451,16 @@ def run_reference(args):
     wl = workload(args.config, 0)
     import oracle
 
-    per_step = 2000 if wl["kind"] == "images" else None
+    per_step = 2000 if wl["kind"] == "images" else (400 if wl["kind"] == "ecfimg" and wl["B"] > 64 else
+                                                     (1 if wl["kind"] == "ecfimg" else None))
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         if wl["kind"] == "images":
             oracle.wect_images(wl["img"][:per_step], wl["dirs"], wl["T"])
+            units = per_step
+        elif wl["kind"] == "ecfimg":
+            oracle.ecf_images(wl["img"][:per_step], wl["T"], 0.0, 255.0)
             units = per_step
         else:
             r = cpu_baseline(wl)
@@ -409,7 +468,7 @@ def run_reference(args):
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append((dt, units, r if units is None else None))
-    if wl["kind"] == "images":
+    if wl["kind"] in ("images", "ecfimg"):
         tot = sum(t for t, _, _ in times)
         value = per_step * len(times) / tot
         sample = f"O2 on images [0, {per_step}) of the {wl['B']}-image workload per step"
@@ -432,7 +491,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4) or ecfx")
+    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4), ecfx, ecfimg or ecfimg1k")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -147,6 +147,27 @@ WECT_API wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, co
 WECT_API wect_status ecf_complex(const wect_complex_desc* K, const float* fvals, int32_t m, const wect_grid* grid,
                         void* out, wect_dtype odtype, void* stream);
 
+/* ECF of a batch of uint8 images (ndim = 2, dims = {H, W}) or voxel volumes (ndim = 3,
+ * dims = {Z, Y, X}): Remark "which-ecf" -- the pixel intensities are the
+ * vertex filter and each entry is the unweighted Euler characteristic of the lower-star
+ * filtration of the image's cubical V-construction (every unit
+ * i-cube a cell of sign (-1)^i, reading A7; a cell's filter value = max of its corners).
+ * This is Algorithm 1 with m = 1 and unit weights, each image its own complex:
+ *     out[b, q] = sum over cells s of image b with max_{v in s} img_b(v) <= beta_b(q) of (-1)^dim s.
+ * Grid (reading A9), in priority order:
+ *   grid->lo < grid->hi  -> the same grid [lo, hi] for every image (e.g. [0, 255] with
+ *                           T = 256: beta(q) = q, one bin per intensity);
+ *   grid->maxheight > 0  -> [-maxheight, maxheight] for every image;
+ *   otherwise            -> the paper's grid [-M_b, M_b], M_b = max intensity of image b
+ *                           (M_b = 0 puts every cell in bin 0, reading A6).
+ * Bins equal the binary64 evaluation of alpha (reading A1), so results are exact integers.
+ * img: [B, dims...] uint8.  dims: HOST array.  grid->d_begin must be 0 and grid->d_count
+ * 0 or 1 (one filter per image); flags other than WECT_TIME_MAIN are ignored.
+ * out: [B, T] of WECT_I32 (refused with WECT_EOVERFLOW when #cells >= 2^31) or WECT_I64.
+ * T in [2, 65536] (WECT_ENOTSUP above).  Errors as for wect_images. */
+WECT_API wect_status ecf_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims,
+                                const wect_grid* grid, void* out, wect_dtype odtype, void* stream);
+
 /* M = max_{p, v} |<l(v), s_p>| over all k0 vertices and all D directions, in binary64
  * (P:624-628), the value wect_complex uses when grid->maxheight <= 0.  Synchronous
  * (writes *M_host).  For direction-sharded runs each rank may call this and the

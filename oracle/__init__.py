@@ -193,3 +193,23 @@ def wect_images(img: np.ndarray, dirs: np.ndarray, T: int, maxheight_override: f
     if rc != 0:
         raise RuntimeError(rc)
     return out
+
+
+def ecf_images(img: np.ndarray, T: int, lo: float = 0.0, hi: float = 0.0, maxheight_override: float = 0.0,
+               naive: bool = False) -> np.ndarray:
+    """O2 (or O1) ECF of a batch [B, dims...] of uint8 images (Remark "which-ecf",
+    P:273-282): per image, the explicit cubical complex with UNIT weights, the
+    intensities as the one vertex filter (fp32, exact), Alg. 1 with m = 1 on the grid
+    [lo, hi] if lo < hi, else [-maxheight, maxheight] if given, else the image's own
+    [-M, M] (P:624-636).  int64 [B, T]."""
+    import synth  # generator container type only
+
+    img = np.ascontiguousarray(img, np.uint8)
+    out = np.zeros((img.shape[0], T), np.int64)
+    for b in range(img.shape[0]):
+        cx = grid_complex(img[b])
+        unit = synth.Complex(cx.coords, None, [synth.Cells(c.verts, None, c.dim) for c in cx.cells], cx.k0,
+                             is_float=False)
+        f = img[b].reshape(-1).astype(np.float32)
+        out[b] = ecf_complex(unit, f, T, lo, hi, maxheight_override, naive)[0]
+    return out

@@ -23,7 +23,7 @@ import numpy as np
 from . import _lib
 from ._lib import FP32_ONLY, TIME_MAIN, VALIDATE, WectError  # noqa: F401
 
-__all__ = ["wect_images", "wect_complex", "ecf_complex", "wect_maxheight", "sync_status", "repair_count",
+__all__ = ["wect_images", "ecf_images", "wect_complex", "ecf_complex", "wect_maxheight", "sync_status", "repair_count",
            "stats", "WectError", "VALIDATE", "FP32_ONLY", "TIME_MAIN", "load"]
 
 load = _lib.load
@@ -116,6 +116,26 @@ def wect_images(img, dirs, T: int, *, d_begin: int = 0, d_count: int = 0, maxhei
     g = _grid(T, d_begin, d_count, maxheight, lo, hi, flags)
     _lib.check(L.wect_images(_ptr(img), B, img.ndim - 1, dims, _ptr(dirs), D, ctypes.byref(g), _ptr(out), odt,
                              _stream(dev, stream)))
+    return out
+
+
+def ecf_images(img, T: int, *, maxheight: float = 0.0, lo: float = 0.0, hi: float = 0.0, out_dtype: str = "int32",
+               out=None, flags: int = 0, stream=None):
+    """ECF of a batch of uint8 images [B, H, W] or volumes [B, Z, Y, X]: intensity as the
+    vertex filter, unweighted lower-star Euler characteristic (Remark "which-ecf",
+    P:273-282).  Grid: [lo, hi] if lo < hi, else [-maxheight, maxheight] if maxheight > 0,
+    else each image's own [-M, M].  Returns [B, T] (int32 or int64)."""
+    L = _lib.load()
+    img = _as(img, np.uint8, "uint8")
+    if img.ndim not in (3, 4):
+        raise ValueError("img must be [B, H, W] or [B, Z, Y, X]")
+    B = int(img.shape[0])
+    dims = (ctypes.c_int64 * (img.ndim - 1))(*[int(d) for d in img.shape[1:]])
+    dev = _device_of(img)
+    out = _alloc_out((B, int(T)), out_dtype, dev, out)
+    odt = {"int32": _lib.I32, "int64": _lib.I64}[out_dtype]
+    g = _grid(T, 0, 0, maxheight, lo, hi, flags)
+    _lib.check(L.ecf_images(_ptr(img), B, img.ndim - 1, dims, ctypes.byref(g), _ptr(out), odt, _stream(dev, stream)))
     return out
 
 

@@ -77,6 +77,10 @@ wect_status launch_absmax_f32(const float* f, int64_t n, unsigned int* bits, cud
 wect_status launch_absmax_i32(const int32_t* w, int64_t n, unsigned int* out, cudaStream_t st, int num_sms);
 wect_status launch_check_indices(const int32_t* v, int64_t n, int64_t k0, unsigned int* flag, cudaStream_t st,
                                  int num_sms);
+size_t ecf_images_scratch_bytes(int64_t B, int64_t nv, int T, bool per_image_M);
+wect_status launch_ecf_images(const uint8_t* img, int64_t B, int ndim, const int64_t* dims, int T, int mode,
+                              double lo, double hi, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
+                              int num_sms);
 wect_status launch_finalize(const void* diff, bool is_float, int64_t rows, int T, void* out, wect_dtype odtype,
                             cudaStream_t st);
 
@@ -312,6 +316,49 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
     }
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
   }
+  if (s != WECT_OK) return s;
+  return out_finish(ov, st);
+}
+
+// -------------------------------------------------------------- image ECF
+wect_status ecf_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims, const wect_grid* grid,
+                       void* out, wect_dtype odtype, void* stream) {
+  g_msg[0] = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!grid) return fail(WECT_EINVAL, "grid is NULL");
+  TimeScope ts(grid->flags);
+  if (ndim != 2 && ndim != 3) return fail(WECT_EINVAL, "ndim must be 2 or 3 (got %d)", ndim);
+  if (!dims) return fail(WECT_EINVAL, "dims is NULL");
+  if (B < 0) return fail(WECT_EINVAL, "B < 0");
+  if (grid->T < 2) return fail(WECT_EINVAL, "T must be >= 2 (beta divides by T-1)");
+  if (grid->T > 65536) return fail(WECT_ENOTSUP, "T > 65536");
+  if (grid->d_begin != 0 || (grid->d_count != 0 && grid->d_count != 1))
+    return fail(WECT_EINVAL, "ecf_images has one filter per image: d_begin must be 0, d_count 0 or 1");
+  int64_t nv = 1, ncells = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (dims[i] < 1) return fail(WECT_EINVAL, "dims[%d] = %lld < 1", i, (long long)dims[i]);
+    if (dims[i] > 65535) return fail(WECT_ENOTSUP, "image side %lld > 65535", (long long)dims[i]);
+    nv *= dims[i];
+    ncells *= 2 * dims[i] - 1;
+  }
+  if (nv > ((int64_t)1 << 34)) return fail(WECT_ENOTSUP, "image of %lld vertices", (long long)nv);
+  if (odtype != WECT_I32 && odtype != WECT_I64) return fail(WECT_EINVAL, "image ECF output must be I32 or I64");
+  if (odtype == WECT_I32 && (double)ncells >= 2147483648.0)
+    return fail(WECT_EOVERFLOW, "int32 output cannot bound %lld cells", (long long)ncells);
+  if (B > 0 && (!img || !out)) return fail(WECT_EINVAL, "img/out is NULL");
+  if (B == 0) return WECT_OK;
+  if (B > 65535 && nv > 4096) return fail(WECT_ENOTSUP, "more than 65535 large images per call");
+  int mode = 0;
+  double lo = 0.0, hi = 0.0;
+  if (grid->lo < grid->hi) { mode = 1; lo = grid->lo; hi = grid->hi; }
+  else if (grid->maxheight > 0) { mode = 1; lo = -grid->maxheight; hi = grid->maxheight; }
+  const int nsm = num_sms_current();
+  Arena ar(st);
+  const uint8_t* dimg = (const uint8_t*)ar.in(img, (size_t)B * nv);
+  OutView ov = out_view(ar, out, (size_t)B * grid->T * dtype_size(odtype));
+  void* scr = ar.alloc(ecf_images_scratch_bytes(B, nv, grid->T, mode == 0));
+  if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging", __FILE__, __LINE__);
+  wect_status s = launch_ecf_images(dimg, B, ndim, dims, grid->T, mode, lo, hi, scr, ov.dev, odtype, st, nsm);
   if (s != WECT_OK) return s;
   return out_finish(ov, st);
 }

@@ -1,0 +1,328 @@
+// k_ecf_images.cu -- ECF of batches of uint8 images / voxel volumes (ecf_images;
+// SURVEY.md §8(f) NEXT-1).
+//
+// What is computed (Remark "which-ecf"): the pixel intensities are the
+// vertex filter and the result is the unweighted Euler characteristic of the lower-star
+// filtration of the cubical V-construction: every axis-aligned
+// unit i-cube of the grid is a cell of sign (-1)^i (reading A7) whose filter
+// value is the max over its corners (lower star).  That is Algorithm 1
+// with m = 1 filter and unit weights, each image its own complex.
+//
+// Intensities are u8, so the method reduces exactly to, per image,
+//   H[c]  = sum over cells with value c of (-1)^dim            (Alg. 1 lines 4-10 by value)
+//   C[c]  = H[0] + ... + H[c]                                 (the sublevel-set EC at c)
+//   out[q] = C[cstar(q)],  cstar(q) = max{c in 0..255 : alpha(c) <= q}   (0 if none)
+// because alpha is monotone (Galois law): the cells in bins <= q are exactly
+// the cells with value <= cstar(q).  cstar is a per-call table evaluated in binary64 in
+// the order alpha is written (reading A1), one row per possible per-image M = 0..255
+// when each image uses its own paper grid [-M, M], else one row.
+//
+// Pairing (fewer shared atomics): the cells anchored at vertex v (v = their lowest
+// corner) are the axis subsets S.  S and S + {x} have opposite signs and
+// value(S + {x}) >= value(S); when the two values are equal they cancel and neither is
+// added.
+//
+// Two paths: images of <= kEcfSmallMax vertices (MNIST-shaped batches): one warp per
+// image, pixels staged in shared memory, a warp-private 256-entry histogram, scan and
+// output in the same warp -- one launch, input read once, output written once.
+// Larger images: CTAs over vertex chunks add their histograms into an int64 [B][256]
+// table (plus the per-image max), then one warp per image scans and maps.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace wect {
+
+constexpr int kEcfWarps = 8;
+constexpr int kEcfSmallMax = 4096;
+constexpr int kEcfChunk = 1 << 15;  // vertices (anchors) per CTA on the large path
+
+// ---------------------------------------------------------------------------
+// cstar table: row r, bin q -> max{c : alpha_r(c) <= q} or -1.
+// mode 0: row r uses the grid [-r, r] (per-image M = r); mode 1: one row, grid [lo, hi].
+// alpha(c) = clamp(ceil(((T-1) (c - lo)) / (hi - lo)), 0, T-1); hi <= lo: bin 0 (A6).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ecf_cstar(int mode, double lo_in, double hi_in, int T,
+                                                   int16_t* __restrict__ cstar) {
+  __shared__ int bins[256];
+  const int r = blockIdx.x;
+  const double lo = mode == 0 ? -(double)r : lo_in;
+  const double hi = mode == 0 ? (double)r : hi_in;
+  {
+    const int c = threadIdx.x;
+    int b = 0;
+    if (hi > lo) {
+      const double u = __ddiv_rn(__dmul_rn((double)(T - 1), __dsub_rn((double)c, lo)), __dsub_rn(hi, lo));
+      const double cu = ceil(u);
+      b = cu < 0.0 ? 0 : (cu > (double)(T - 1) ? T - 1 : (int)cu);
+    }
+    bins[c] = b;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < T; q += blockDim.x) {
+    // bins[] is non-decreasing in c: count = #{c : bins[c] <= q} by binary search
+    int lo_i = 0, hi_i = 256;
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i) >> 1;
+      if (bins[mid] <= q) lo_i = mid + 1;
+      else hi_i = mid;
+    }
+    cstar[(int64_t)r * T + q] = (int16_t)(lo_i - 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Signed cell values of the cells anchored at vertex v (see "Pairing" above).
+// p: the image's pixels; (x, y, z): v's coordinates; X, Y, Z: dims (Z = 1 in 2D);
+// add(c, s): histogram update.
+// ---------------------------------------------------------------------------
+template <int ND, typename Px, typename Add>
+__device__ __forceinline__ void ecf_anchor(Px p, int64_t v, int x, int y, int z, int X, int Y, int Z, Add add) {
+  const bool ex = x + 1 < X, ey = y + 1 < Y, ez = ND == 3 && z + 1 < Z;
+  const int64_t sy = X, sz = (int64_t)X * Y;
+  // face maxima at x (f) and at x + 1 (g) for S in {}, {y}, {z}, {y,z}
+  const int a = p(v), a1 = ex ? p(v + 1) : 0;
+  int f[4], g[4];
+  f[0] = a;
+  g[0] = a1;
+  if (ey) {
+    f[1] = max(a, p(v + sy));
+    g[1] = ex ? max(a1, p(v + 1 + sy)) : 0;
+  }
+  if (ND == 3 && ez) {
+    f[2] = max(a, p(v + sz));
+    g[2] = ex ? max(a1, p(v + 1 + sz)) : 0;
+    if (ey) {
+      f[3] = max(max(f[1], f[2]), p(v + sy + sz));
+      g[3] = ex ? max(max(g[1], g[2]), p(v + 1 + sy + sz)) : 0;
+    }
+  }
+#pragma unroll
+  for (int S = 0; S < (ND == 3 ? 4 : 2); ++S) {
+    const bool valid = (!(S & 1) || ey) && (!(S & 2) || ez);
+    if (!valid) continue;
+    const int s = (__popc(S) & 1) ? -1 : 1;  // (-1)^|S|
+    const int m = f[S];
+    if (ex) {
+      const int mx = max(m, g[S]);
+      if (mx != m) {
+        add(m, s);
+        add(mx, -s);
+      }
+    } else {
+      add(m, s);
+    }
+  }
+}
+
+// Per-image tail (one warp): in-place scan of the 256-entry histogram and the mapped
+// output row.  hist: shared, 256 entries of Acc.
+template <typename Acc, typename OutT>
+__device__ __forceinline__ void ecf_scan_emit(Acc* hist, int lane, const int16_t* __restrict__ cst, int T,
+                                              OutT* __restrict__ orow) {
+  Acc loc[8];
+  Acc run = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    run += hist[8 * lane + k];
+    loc[k] = run;
+  }
+  Acc incl = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Acc y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const Acc excl = incl - run;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) hist[8 * lane + k] = excl + loc[k];
+  __syncwarp();
+  for (int q = lane; q < T; q += 32) {
+    const int cs = __ldg(cst + q);
+    orow[q] = (OutT)(cs >= 0 ? hist[cs] : (Acc)0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Small images: one warp per image.
+// smem per warp: hist[256] int32, then the image's pixels (HW bytes, 16-byte aligned).
+// ---------------------------------------------------------------------------
+template <int ND, typename OutT>
+__global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img_small(const uint8_t* __restrict__ img, int64_t B, int X,
+                                                                  int Y, int Z, int per_image_M,
+                                                                  const int16_t* __restrict__ cstar, int T,
+                                                                  OutT* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int HW = X * Y * Z;
+  const int pbytes = (HW + 15) & ~15;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* hist = (int*)(smem + (size_t)warp * (1024 + pbytes));
+  uint8_t* pix = (uint8_t*)(hist + 256);
+  const bool vec = (HW & 15) == 0 && ((uintptr_t)img & 15) == 0;
+  const int64_t nwarps = (int64_t)gridDim.x * kEcfWarps;
+  for (int64_t b = (int64_t)blockIdx.x * kEcfWarps + warp; b < B; b += nwarps) {
+    const uint8_t* src = img + b * HW;
+    unsigned mx = 0;
+    if (vec) {
+      for (int i = lane; i < (HW >> 4); i += 32) {
+        const uint4 w = __ldcs((const uint4*)src + i);
+        *((uint4*)pix + i) = w;
+        mx = __vmaxu4(mx, __vmaxu4(__vmaxu4(w.x, w.y), __vmaxu4(w.z, w.w)));
+      }
+    } else {
+      for (int i = lane; i < HW; i += 32) {
+        const uint8_t w = src[i];
+        pix[i] = w;
+        mx = w > mx ? w : mx;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hist[8 * lane + k] = 0;
+    mx = max(max(mx & 0xFFu, (mx >> 8) & 0xFFu), max((mx >> 16) & 0xFFu, mx >> 24));
+    const int M = (int)__reduce_max_sync(0xffffffffu, mx);
+    __syncwarp();
+    const uint32_t hs = (uint32_t)__cvta_generic_to_shared(hist);
+    auto px = [&](int64_t u) -> int { return pix[u]; };
+    auto add = [&](int c, int s) { asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(hs + 4u * c), "r"(s) : "memory"); };
+    int x = lane % X, yz = lane / X;
+    int y = yz % Y, z = yz / Y;
+    const int sx = 32 % X, syz = 32 / X;
+    for (int v = lane; v < HW; v += 32) {
+      ecf_anchor<ND>(px, v, x, y, z, X, Y, Z, add);
+      x += sx;
+      y += syz;
+      if (x >= X) { x -= X; ++y; }
+      while (y >= Y) { y -= Y; ++z; }
+    }
+    __syncwarp();
+    ecf_scan_emit<int, OutT>(hist, lane, cstar + (per_image_M ? (int64_t)M * T : 0), T, out + b * T);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Large images: CTA (chunk, image) -> int64 histogram table [B][256] and per-image max.
+// ---------------------------------------------------------------------------
+template <int ND>
+__global__ void __launch_bounds__(256) k_ecf_img_hist(const uint8_t* __restrict__ img, int X, int Y, int Z,
+                                                      unsigned long long* __restrict__ ghist,
+                                                      unsigned int* __restrict__ gmax) {
+  __shared__ int hist[kEcfWarps][256];
+  __shared__ unsigned int smax;
+  const int64_t HW = (int64_t)X * Y * Z;
+  const int64_t b = blockIdx.y;
+  const int64_t v0 = (int64_t)blockIdx.x * kEcfChunk;
+  const int64_t v1 = v0 + kEcfChunk < HW ? v0 + kEcfChunk : HW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kEcfWarps * 256; i += blockDim.x) (&hist[0][0])[i] = 0;
+  if (threadIdx.x == 0) smax = 0;
+  __syncthreads();
+  const uint8_t* src = img + b * HW;
+  const uint32_t hs = (uint32_t)__cvta_generic_to_shared(&hist[warp][0]);
+  auto px = [&](int64_t u) -> int { return __ldg(src + u); };
+  auto add = [&](int c, int s) { asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(hs + 4u * c), "r"(s) : "memory"); };
+  unsigned mx = 0;
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    const int x = (int)(v % X);
+    const int64_t yz = v / X;
+    const int y = (int)(yz % Y), z = (int)(yz / Y);
+    ecf_anchor<ND>(px, v, x, y, z, X, Y, Z, add);
+    const unsigned a = src[v];
+    mx = a > mx ? a : mx;
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) atomicMax(&smax, mx);
+  __syncthreads();
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < kEcfWarps; ++w) s += hist[w][c];
+    if (s != 0) atomicAdd(ghist + b * 256 + c, (unsigned long long)(long long)s);
+  }
+  if (threadIdx.x == 0) atomicMax(gmax + b, smax);
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img_final(const unsigned long long* __restrict__ ghist,
+                                                                  const unsigned int* __restrict__ gmax, int64_t B,
+                                                                  int per_image_M, const int16_t* __restrict__ cstar,
+                                                                  int T, OutT* __restrict__ out) {
+  __shared__ long long hist[kEcfWarps][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * kEcfWarps + warp;
+  if (b >= B) return;
+  for (int c = lane; c < 256; c += 32) hist[warp][c] = (long long)ghist[b * 256 + c];
+  __syncwarp();
+  const int M = per_image_M ? (int)gmax[b] : 0;
+  ecf_scan_emit<long long, OutT>(&hist[warp][0], lane, cstar + (int64_t)M * T, T, out + b * T);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+size_t ecf_images_scratch_bytes(int64_t B, int64_t nv, int T, bool per_image_M) {
+  size_t s = (size_t)(per_image_M ? 256 : 1) * T * sizeof(int16_t);
+  s = (s + 255) & ~(size_t)255;
+  if (nv > kEcfSmallMax) s += (size_t)B * 256 * 8 + (size_t)B * 4 + 256;
+  return s;
+}
+
+template <typename OutT>
+static wect_status launch_ecf_images_t(const uint8_t* img, int64_t B, int ndim, const int64_t* dims, int T, int mode,
+                                       double lo, double hi, void* scratch, OutT* out, cudaStream_t st, int num_sms) {
+  // dims: {H, W} or {Z, Y, X}; X is the fastest axis
+  const int X = (int)dims[ndim - 1], Y = (int)dims[ndim - 2], Z = ndim == 3 ? (int)dims[0] : 1;
+  const int64_t nv = (int64_t)X * Y * Z;
+  const int per_image_M = mode == 0;
+  int16_t* cstar = (int16_t*)scratch;
+  k_ecf_cstar<<<per_image_M ? 256 : 1, 256, 0, st>>>(mode, lo, hi, T, cstar); count_launch();
+  WECT_CUDA_TRY(cudaGetLastError());
+  size_t off = ((size_t)(per_image_M ? 256 : 1) * T * sizeof(int16_t) + 255) & ~(size_t)255;
+  if (nv <= kEcfSmallMax) {
+    const int pbytes = (int)((nv + 15) & ~15);
+    const size_t smem = (size_t)kEcfWarps * (1024 + pbytes);
+    const int64_t ctas_needed = (B + kEcfWarps - 1) / kEcfWarps;
+    int per_sm = (int)((200 * 1024) / smem);
+    per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+    const int64_t cap = (int64_t)num_sms * per_sm;
+    const int grid = (int)(ctas_needed < cap ? ctas_needed : cap);
+    MainTimer timer(st);
+    if (ndim == 2) {
+      WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf_img_small<2, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_ecf_img_small<2, OutT><<<grid, kEcfWarps * 32, smem, st>>>(img, B, X, Y, 1, per_image_M, cstar, T, out);
+    } else {
+      WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf_img_small<3, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_ecf_img_small<3, OutT><<<grid, kEcfWarps * 32, smem, st>>>(img, B, X, Y, Z, per_image_M, cstar, T, out);
+    }
+    count_launch();
+    timer.stop();
+    WECT_CUDA_TRY(cudaGetLastError());
+    return WECT_OK;
+  }
+  unsigned long long* ghist = (unsigned long long*)((char*)scratch + off);
+  unsigned int* gmax = (unsigned int*)(ghist + (size_t)B * 256);
+  WECT_CUDA_TRY(cudaMemsetAsync(ghist, 0, (size_t)B * 256 * 8 + (size_t)B * 4, st));
+  dim3 g((unsigned)((nv + kEcfChunk - 1) / kEcfChunk), (unsigned)B);
+  {
+    MainTimer timer(st);
+    if (ndim == 2) k_ecf_img_hist<2><<<g, 256, 0, st>>>(img, X, Y, 1, ghist, gmax);
+    else k_ecf_img_hist<3><<<g, 256, 0, st>>>(img, X, Y, Z, ghist, gmax);
+    count_launch();
+    timer.stop();
+  }
+  WECT_CUDA_TRY(cudaGetLastError());
+  k_ecf_img_final<OutT><<<(unsigned)((B + kEcfWarps - 1) / kEcfWarps), kEcfWarps * 32, 0, st>>>(
+      ghist, gmax, B, per_image_M, cstar, T, out); count_launch();
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+wect_status launch_ecf_images(const uint8_t* img, int64_t B, int ndim, const int64_t* dims, int T, int mode,
+                              double lo, double hi, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
+                              int num_sms) {
+  if (odtype == WECT_I32)
+    return launch_ecf_images_t<int32_t>(img, B, ndim, dims, T, mode, lo, hi, scratch, (int32_t*)out, st, num_sms);
+  return launch_ecf_images_t<long long>(img, B, ndim, dims, T, mode, lo, hi, scratch, (long long*)out, st, num_sms);
+}
+
+}  // namespace wect
