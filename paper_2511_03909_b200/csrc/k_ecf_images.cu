@@ -22,7 +22,9 @@
 // value(S + {x}) >= value(S); when the two values are equal they cancel and neither is
 // added.
 //
-// Two paths: images of <= kEcfSmallMax vertices (MNIST-shaped batches): one warp per
+// Three paths: 2-D images with W % 4 == 0, H*W % 16 == 0, H*W <= kEcfSmallMax (the
+// MNIST-shaped batches): k_ecf_img2d_w4, packed u16x2 (below).  Other images of
+// <= kEcfSmallMax vertices (MNIST-shaped batches): one warp per
 // image, pixels staged in shared memory, a warp-private 256-entry histogram, scan and
 // output in the same warp -- one launch, input read once, output written once.
 // Larger images: CTAs over vertex chunks add their histograms into an int64 [B][256]
@@ -201,6 +203,122 @@ __global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img_small(const uint8_t*
 }
 
 // ---------------------------------------------------------------------------
+// Small 2-D images with W % 4 == 0 (MNIST-shaped): packed u16x2 form of the same pairing.
+// The image is staged as u16 values 4*p (byte offsets into the histogram) in rows of
+// pitch P = W + 2 with one extra row; the padding column(s) and row hold 4*256, a sink bin
+// past the 256 real ones.  Then every anchor is handled alike: a missing x-neighbour
+// makes max(a, b) the sink (so +1@a, -1@sink), a missing y-row makes both y-cells the
+// sink (they cancel).  A lane takes two anchors (x, x+1) per step: four 32-bit LDS, two
+// byte permutes and three u16x2 maxima give a, max(a,b), max(a,c), max(a,b,c,d) for both.
+// The warp's histogram sits at a 2048-byte aligned shared address (aligned at run time
+// inside the dynamic window) so each histogram address is one LOP3 of the packed value.
+// ---------------------------------------------------------------------------
+constexpr int kSinkOff = 4 * 256;
+
+template <typename OutT>
+__global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img2d_w4(const uint8_t* __restrict__ img, int64_t B, int H,
+                                                                 int W, int per_image_M,
+                                                                 const int16_t* __restrict__ cstar, int T,
+                                                                 OutT* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = W + 2, P2 = P >> 1, W2 = W >> 1, HW = H * W;
+  const int pwords = (H + 1) * P2;
+  // [pad to a 2048-byte aligned shared address][kEcfWarps x 2048-byte histograms][pixels]
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
+  unsigned char* hbase = smem + (((s0 + 2047u) & ~2047u) - s0);
+  int* hist = (int*)(hbase + (size_t)warp * 2048);
+  uint32_t* S = (uint32_t*)(hbase + kEcfWarps * 2048) + (size_t)warp * ((pwords + 3) & ~3);
+  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(hist);
+  for (int i = lane; i < pwords; i += 32) S[i] = (uint32_t)kSinkOff | ((uint32_t)kSinkOff << 16);
+  const float invW = 1.0f / (float)W, invW2 = 1.0f / (float)W2;
+  // the fixed grid's cstar row in registers (T <= 256)
+  int creg[8];
+  const bool creg_ok = !per_image_M && T <= 256;
+  if (creg_ok) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) creg[k] = 32 * k + lane < T ? (int)__ldg(cstar + 32 * k + lane) : -1;
+  }
+  __syncwarp();
+  const int64_t nwarps = (int64_t)gridDim.x * kEcfWarps;
+  for (int64_t b = (int64_t)blockIdx.x * kEcfWarps + warp; b < B; b += nwarps) {
+    const uint4* src = (const uint4*)(img + b * HW);
+    unsigned mx = 0;
+    for (int i = lane; i < (HW >> 4); i += 32) {
+      const uint4 w = __ldcs(src + i);
+      const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int v = 16 * i + 4 * g;
+        const int r = (int)(((float)v + 0.5f) * invW);
+        const int widx = (r * P + (v - r * W)) >> 1;
+        S[widx] = __byte_perm(wv[g], 0, 0x4140) << 2;
+        S[widx + 1] = __byte_perm(wv[g], 0, 0x4342) << 2;
+        mx = __vmaxu4(mx, wv[g]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hist[8 * lane + k] = 0;
+    mx = max(max(mx & 0xFFu, (mx >> 8) & 0xFFu), max((mx >> 16) & 0xFFu, mx >> 24));
+    const int M = (int)__reduce_max_sync(0xffffffffu, mx);
+    __syncwarp();
+    for (int it = lane; it < H * W2; it += 32) {
+      const int r = (int)(((float)it + 0.5f) * invW2);
+      const int ai = r * P2 + (it - r * W2);
+      const uint32_t a2 = S[ai], an = S[ai + 1], c2 = S[ai + P2], cn = S[ai + P2 + 1];
+      const uint32_t b2 = __byte_perm(a2, an, 0x5432), d2 = __byte_perm(c2, cn, 0x5432);
+      const uint32_t m_x = __vmaxu2(a2, b2), m_y = __vmaxu2(a2, c2);
+      const uint32_t m_xy = __vmaxu2(m_x, __vmaxu2(c2, d2));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t A = (h ? a2 >> 16 : a2 & 0xFFFFu) | wbase;
+        const uint32_t X = (h ? m_x >> 16 : m_x & 0xFFFFu) | wbase;
+        const uint32_t Y = (h ? m_y >> 16 : m_y & 0xFFFFu) | wbase;
+        const uint32_t XY = (h ? m_xy >> 16 : m_xy & 0xFFFFu) | wbase;
+        if (X != A) {
+          asm volatile("red.shared.add.s32 [%0], 1;" ::"r"(A) : "memory");
+          asm volatile("red.shared.add.s32 [%0], -1;" ::"r"(X) : "memory");
+        }
+        if (XY != Y) {
+          asm volatile("red.shared.add.s32 [%0], -1;" ::"r"(Y) : "memory");
+          asm volatile("red.shared.add.s32 [%0], 1;" ::"r"(XY) : "memory");
+        }
+      }
+    }
+    __syncwarp();
+    // in-place inclusive scan of the 256 real bins (lane: bins 8l .. 8l+7)
+    int4 h0 = *(int4*)(hist + 8 * lane), h1 = *(int4*)(hist + 8 * lane + 4);
+    h0.y += h0.x; h0.z += h0.y; h0.w += h0.z;
+    h1.x += h0.w; h1.y += h1.x; h1.z += h1.y; h1.w += h1.z;
+    int incl = h1.w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int ex = incl - h1.w;
+    h0.x += ex; h0.y += ex; h0.z += ex; h0.w += ex;
+    h1.x += ex; h1.y += ex; h1.z += ex; h1.w += ex;
+    *(int4*)(hist + 8 * lane) = h0;
+    *(int4*)(hist + 8 * lane + 4) = h1;
+    __syncwarp();
+    OutT* orow = out + b * T;
+    if (creg_ok) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (32 * k + lane < T) __stcs(orow + 32 * k + lane, (OutT)(creg[k] >= 0 ? hist[creg[k]] : 0));
+    } else {
+      const int16_t* cst = cstar + (per_image_M ? (int64_t)M * T : 0);
+      for (int q = lane; q < T; q += 32) {
+        const int cs = __ldg(cst + q);
+        orow[q] = (OutT)(cs >= 0 ? hist[cs] : 0);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Large images: CTA (chunk, image) -> int64 histogram table [B][256] and per-image max.
 // ---------------------------------------------------------------------------
 template <int ND>
@@ -278,6 +396,20 @@ static wect_status launch_ecf_images_t(const uint8_t* img, int64_t B, int ndim, 
   k_ecf_cstar<<<per_image_M ? 256 : 1, 256, 0, st>>>(mode, lo, hi, T, cstar); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   size_t off = ((size_t)(per_image_M ? 256 : 1) * T * sizeof(int16_t) + 255) & ~(size_t)255;
+  if (ndim == 2 && X % 4 == 0 && X <= 256 && nv <= kEcfSmallMax && nv % 16 == 0 && ((uintptr_t)img & 15) == 0) {
+    const int pwords = (Y + 1) * ((X + 2) >> 1);
+    const size_t smem = (size_t)kEcfWarps * ((pwords + 3) & ~3) * 4 + 2048 + (size_t)kEcfWarps * 2048;
+    const int64_t ctas_needed = (B + kEcfWarps - 1) / kEcfWarps;
+    const int64_t cap = (int64_t)num_sms * 8;
+    const int grid = (int)(ctas_needed < cap ? ctas_needed : cap);
+    MainTimer timer(st);
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf_img2d_w4<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ecf_img2d_w4<OutT><<<grid, kEcfWarps * 32, smem, st>>>(img, B, Y, X, per_image_M, cstar, T, out);
+    count_launch();
+    timer.stop();
+    WECT_CUDA_TRY(cudaGetLastError());
+    return WECT_OK;
+  }
   if (nv <= kEcfSmallMax) {
     const int pbytes = (int)((nv + 15) & ~15);
     const size_t smem = (size_t)kEcfWarps * (1024 + pbytes);

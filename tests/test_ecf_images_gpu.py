@@ -33,7 +33,9 @@ def _orc(img, T, g):
 
 
 @pytest.mark.parametrize("dims,B,T", [((28, 28), 70, 256), ((5, 7), 33, 13), ((1, 9), 5, 6), ((9, 1), 4, 5),
-                                      ((1, 1), 3, 2), ((64, 64), 9, 100), ((70, 80), 3, 256), ((3, 300), 2, 64)])
+                                      ((1, 1), 3, 2), ((64, 64), 9, 100), ((70, 80), 3, 256), ((3, 300), 2, 64),
+                                      ((5, 8), 40, 256), ((4, 12), 37, 31), ((7, 12), 6, 256), ((1, 16), 9, 20),
+                                      ((16, 4), 9, 20)])
 @pytest.mark.parametrize("gi", range(len(GRIDS)))
 def test_ecf_images_2d_vs_O2(dims, B, T, gi):
     img = synth.images_u8(B, dims, 500 + dims[0] * 7 + dims[1] + gi)
