@@ -22,7 +22,7 @@
 // value(S + {x}) >= value(S); when the two values are equal they cancel and neither is
 // added.
 //
-// Three paths: 2-D images with W % 4 == 0, H*W % 16 == 0, H*W <= kEcfSmallMax (the
+// Three paths: 2-D images with W % 4 == 0, H*W % 16 == 0, H*W <= 1024 (the
 // MNIST-shaped batches): k_ecf_img2d_w4, packed u16x2 (below).  Other images of
 // <= kEcfSmallMax vertices (MNIST-shaped batches): one warp per
 // image, pixels staged in shared memory, a warp-private 256-entry histogram, scan and
@@ -231,7 +231,6 @@ __global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img2d_w4(const uint8_t* 
   uint32_t* S = (uint32_t*)(hbase + kEcfWarps * 2048) + (size_t)warp * ((pwords + 3) & ~3);
   const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(hist);
   for (int i = lane; i < pwords; i += 32) S[i] = (uint32_t)kSinkOff | ((uint32_t)kSinkOff << 16);
-  const float invW = 1.0f / (float)W, invW2 = 1.0f / (float)W2;
   // the fixed grid's cstar row in registers (T <= 256)
   int creg[8];
   const bool creg_ok = !per_image_M && T <= 256;
@@ -241,30 +240,55 @@ __global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img2d_w4(const uint8_t* 
   }
   __syncwarp();
   const int64_t nwarps = (int64_t)gridDim.x * kEcfWarps;
-  for (int64_t b = (int64_t)blockIdx.x * kEcfWarps + warp; b < B; b += nwarps) {
-    const uint4* src = (const uint4*)(img + b * HW);
-    unsigned mx = 0;
-    for (int i = lane; i < (HW >> 4); i += 32) {
-      const uint4 w = __ldcs(src + i);
-      const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  const int n16 = HW >> 4;  // <= 64: at most two 16-byte loads per lane
+  // lane's two 16-pixel blocks: flat pixel index -> staged word index (row pitch P)
+  int widx[2][4];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int v = 16 * i + 4 * g;
-        const int r = (int)(((float)v + 0.5f) * invW);
-        const int widx = (r * P + (v - r * W)) >> 1;
-        S[widx] = __byte_perm(wv[g], 0, 0x4140) << 2;
-        S[widx + 1] = __byte_perm(wv[g], 0, 0x4342) << 2;
-        mx = __vmaxu4(mx, wv[g]);
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int v = 16 * (lane + 32 * j) + 4 * g;
+      const int r = v / W;
+      widx[j][g] = (r * P + (v - r * W)) >> 1;
+    }
+  // anchor-pair coordinates advance by 32 items per step: (dr, dx) = divmod(32, W2)
+  const int dr = 32 / W2, dx = 32 - dr * W2;
+  const int r0 = lane / W2, x0 = lane - r0 * W2;
+  int64_t b = (int64_t)blockIdx.x * kEcfWarps + warp;
+  uint4 pf[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    pf[j] = (b < B && lane + 32 * j < n16) ? __ldcs((const uint4*)(img + b * HW) + lane + 32 * j) : make_uint4(0, 0, 0, 0);
+  for (; b < B; b += nwarps) {
+    unsigned mx = 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (lane + 32 * j < n16) {
+        const uint32_t wv[4] = {pf[j].x, pf[j].y, pf[j].z, pf[j].w};
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          S[widx[j][g]] = __byte_perm(wv[g], 0, 0x4140) << 2;
+          S[widx[j][g] + 1] = __byte_perm(wv[g], 0, 0x4342) << 2;
+          mx = __vmaxu4(mx, wv[g]);
+        }
       }
     }
+    // the next image's pixels are in flight while this one is processed
+    const int64_t bn = b + nwarps;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (bn < B && lane + 32 * j < n16) pf[j] = __ldcs((const uint4*)(img + bn * HW) + lane + 32 * j);
 #pragma unroll
     for (int k = 0; k < 8; ++k) hist[8 * lane + k] = 0;
     mx = max(max(mx & 0xFFu, (mx >> 8) & 0xFFu), max((mx >> 16) & 0xFFu, mx >> 24));
     const int M = (int)__reduce_max_sync(0xffffffffu, mx);
     __syncwarp();
+    int r = r0, xp = x0;
     for (int it = lane; it < H * W2; it += 32) {
-      const int r = (int)(((float)it + 0.5f) * invW2);
-      const int ai = r * P2 + (it - r * W2);
+      const int ai = r * P2 + xp;
+      xp += dx;
+      r += dr;
+      if (xp >= W2) { xp -= W2; ++r; }
       const uint32_t a2 = S[ai], an = S[ai + 1], c2 = S[ai + P2], cn = S[ai + P2 + 1];
       const uint32_t b2 = __byte_perm(a2, an, 0x5432), d2 = __byte_perm(c2, cn, 0x5432);
       const uint32_t m_x = __vmaxu2(a2, b2), m_y = __vmaxu2(a2, c2);
@@ -275,6 +299,7 @@ __global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img2d_w4(const uint8_t* 
         const uint32_t X = (h ? m_x >> 16 : m_x & 0xFFFFu) | wbase;
         const uint32_t Y = (h ? m_y >> 16 : m_y & 0xFFFFu) | wbase;
         const uint32_t XY = (h ? m_xy >> 16 : m_xy & 0xFFFFu) | wbase;
+        // equal values cancel and are skipped
         if (X != A) {
           asm volatile("red.shared.add.s32 [%0], 1;" ::"r"(A) : "memory");
           asm volatile("red.shared.add.s32 [%0], -1;" ::"r"(X) : "memory");
@@ -396,7 +421,7 @@ static wect_status launch_ecf_images_t(const uint8_t* img, int64_t B, int ndim, 
   k_ecf_cstar<<<per_image_M ? 256 : 1, 256, 0, st>>>(mode, lo, hi, T, cstar); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   size_t off = ((size_t)(per_image_M ? 256 : 1) * T * sizeof(int16_t) + 255) & ~(size_t)255;
-  if (ndim == 2 && X % 4 == 0 && X <= 256 && nv <= kEcfSmallMax && nv % 16 == 0 && ((uintptr_t)img & 15) == 0) {
+  if (ndim == 2 && X % 4 == 0 && nv <= 1024 && nv % 16 == 0 && ((uintptr_t)img & 15) == 0) {
     const int pwords = (Y + 1) * ((X + 2) >> 1);
     const size_t smem = (size_t)kEcfWarps * ((pwords + 3) & ~3) * 4 + 2048 + (size_t)kEcfWarps * 2048;
     const int64_t ctas_needed = (B + kEcfWarps - 1) / kEcfWarps;
