@@ -168,6 +168,30 @@ WECT_API wect_status ecf_complex(const wect_complex_desc* K, const float* fvals,
 WECT_API wect_status ecf_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims,
                                 const wect_grid* grid, void* out, wect_dtype odtype, void* stream);
 
+/* Gradient of a scalar loss L with respect to the weights, through wect_complex /
+ * ecf_complex (the paper's differentiability claim).
+ * Alg. 1 is linear in the weights (closed form P:769-776), so with G = dL/dout,
+ *     dL/dw(s) = (-1)^dim s * sum_p sum_{q >= bin(s, p)} G[p, q]
+ * where bin(s, p) is the forward's cell bin (max of its vertices' alpha, eq. msi P:713-723,
+ * evaluated exactly per reading A1).  Coordinates / filter values receive no gradient
+ * (the output is piecewise constant in them).
+ * K, dirs / fvals, D / m, grid: exactly as for the forward call (M over ALL rows, A2);
+ *   K->wdtype and the weight arrays are not read.
+ * G: [d_count, T] fp64, the rows d_begin .. d_begin + d_count of dL/dout.
+ * grad_vweights: [k0] fp64 output or NULL (skip).
+ * grad_cells: HOST array of K->ncell_dims pointers (or NULL), entry i an [cells[i].count] fp64
+ *   output or NULL (skip).  Outputs are overwritten.  Cells of arity > 8: WECT_ENOTSUP.
+ * Accumulation: RC = reverse cumsum of each G row in binary64 from q = T-1 down, then the
+ *   sum over rows in a fixed order (tiles of 32 rows; a shuffle tree within a tile):
+ *   deterministic, within binary64 rounding of the exact sum (reading A13).
+ * Errors as for wect_complex; an out-of-range vertex index is reported by wect_sync_status. */
+WECT_API wect_status wect_complex_backward(const wect_complex_desc* K, const float* dirs, int32_t D,
+                                           const wect_grid* grid, const double* G, double* grad_vweights,
+                                           double* const* grad_cells, void* stream);
+WECT_API wect_status ecf_complex_backward(const wect_complex_desc* K, const float* fvals, int32_t m,
+                                          const wect_grid* grid, const double* G, double* grad_vweights,
+                                          double* const* grad_cells, void* stream);
+
 /* M = max_{p, v} |<l(v), s_p>| over all k0 vertices and all D directions, in binary64
  * (P:624-628), the value wect_complex uses when grid->maxheight <= 0.  Synchronous
  * (writes *M_host).  For direction-sharded runs each rank may call this and the

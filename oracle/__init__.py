@@ -213,3 +213,55 @@ def ecf_images(img: np.ndarray, T: int, lo: float = 0.0, hi: float = 0.0, maxhei
         f = img[b].reshape(-1).astype(np.float32)
         out[b] = ecf_complex(unit, f, T, lo, hi, maxheight_override, naive)[0]
     return out
+
+
+# ------------------------------------------------------- weights gradient (NEXT-3)
+def alpha_vec(t: np.ndarray, lo: float, hi: float, T: int) -> np.ndarray:
+    """alpha (eq. left-adjoint) elementwise in binary64, in the written order:
+    u = ((T-1) * (t - lo)) / (hi - lo), clamp(ceil(u), 0, T-1); hi <= lo -> 0 (reading A6)."""
+    t = np.asarray(t, np.float64)
+    if not hi > lo:
+        return np.zeros(t.shape, np.int64)
+    u = (float(T - 1) * (t - lo)) / (hi - lo)
+    return np.clip(np.ceil(u), 0, T - 1).astype(np.int64)
+
+
+def wecfs_grad(fvals: np.ndarray, cx, T: int, lo: float, hi: float, G: np.ndarray):
+    """dL/dw for L with G = dL/dWECFs [m, T], straight from the closed form:
+    WECFs[p, q] = sum_s w(s) (-1)^dim s [bin(s, p) <= q], bin(s, p) = max over the vertices
+    of s of alpha(f_p(v)) (Alg. 1 lines 3, 7-8), so
+        dL/dw(s) = sum_{p, q} G[p, q] (-1)^dim s [bin(s, p) <= q].
+    The indicator is materialised ([cells, m, T]) -- small inputs only.
+    Returns (grad_vweights [k0], [grad_cells_i]) in float64."""
+    fv = np.asarray(fvals, np.float64)
+    G = np.asarray(G, np.float64)
+    vb = alpha_vec(fv, lo, hi, T)  # [k0, m]
+    q = np.arange(T)
+
+    def grad_of(bins, sign):  # bins [count, m]
+        ind = (bins[:, :, None] <= q[None, None, :]).astype(np.float64)
+        return sign * np.einsum("spq,pq->s", ind, G)
+
+    gv = grad_of(vb, 1.0)
+    gc = []
+    for c in cx.cells:
+        v = np.asarray(c.verts, np.int64).reshape(len(c.verts), -1)
+        gc.append(grad_of(vb[v].max(axis=1), -1.0 if c.dim % 2 else 1.0))
+    return gv, gc
+
+
+def wect_complex_grad(cx, dirs: np.ndarray, T: int, G: np.ndarray, maxheight_override: float = 0.0):
+    """Weights gradient through wect_complex (M over ALL directions, reading A2)."""
+    fv = heights(cx.coords, dirs)
+    M = maxheight_override if maxheight_override > 0 else maxheight(fv)
+    return wecfs_grad(fv, cx, T, -M, M, G)
+
+
+def ecf_complex_grad(cx, fvals32: np.ndarray, T: int, G: np.ndarray, lo: float = 0.0, hi: float = 0.0):
+    fv = np.ascontiguousarray(fvals32, np.float32).astype(np.float64)
+    if fv.ndim == 1:
+        fv = fv[:, None]
+    if not lo < hi:
+        M = maxheight(fv)
+        lo, hi = -M, M
+    return wecfs_grad(fv, cx, T, lo, hi, G)

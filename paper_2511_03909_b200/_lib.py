@@ -18,7 +18,7 @@ U8, I32, I64, F32, F64 = 1, 2, 3, 4, 5
 # flags
 VALIDATE, FP32_ONLY, TIME_MAIN = 1, 2, 4
 
-EXPORTS = ("wect_complex", "wect_images", "ecf_complex", "ecf_images", "wect_maxheight", "wect_sync_status", "wect_last_error",
+EXPORTS = ("wect_complex", "wect_images", "ecf_complex", "ecf_images", "wect_complex_backward", "ecf_complex_backward", "wect_maxheight", "wect_sync_status", "wect_last_error",
            "wect_repair_count", "wect_stats", "wect_abi_version")
 
 
@@ -61,11 +61,14 @@ def load() -> ctypes.CDLL:
     L.ecf_complex.argtypes = L.wect_complex.argtypes
     L.wect_images.argtypes = [vp, i64, i32, vp, vp, i32, ctypes.POINTER(wect_grid), vp, ctypes.c_int, vp]
     L.ecf_images.argtypes = [vp, i64, i32, vp, ctypes.POINTER(wect_grid), vp, ctypes.c_int, vp]
+    L.wect_complex_backward.argtypes = [ctypes.POINTER(wect_complex_desc), vp, i32, ctypes.POINTER(wect_grid), vp, vp,
+                                        vp, vp]
+    L.ecf_complex_backward.argtypes = L.wect_complex_backward.argtypes
     L.wect_maxheight.argtypes = [vp, i64, i32, vp, i32, ctypes.POINTER(ctypes.c_double), vp]
     L.wect_sync_status.argtypes = [vp]
     L.wect_last_error.restype = ctypes.c_char_p
     L.wect_repair_count.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
-    for f in ("wect_complex", "ecf_complex", "wect_images", "ecf_images", "wect_maxheight", "wect_sync_status", "wect_repair_count"):
+    for f in ("wect_complex", "ecf_complex", "wect_images", "ecf_images", "wect_complex_backward", "ecf_complex_backward", "wect_maxheight", "wect_sync_status", "wect_repair_count"):
         getattr(L, f).restype = ctypes.c_int
     L.wect_stats.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                              ctypes.POINTER(ctypes.c_double), ctypes.c_int]

@@ -81,6 +81,9 @@ size_t ecf_images_scratch_bytes(int64_t B, int64_t nv, int T, bool per_image_M);
 wect_status launch_ecf_images(const uint8_t* img, int64_t B, int ndim, const int64_t* dims, int T, int mode,
                               double lo, double hi, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                               int num_sms);
+wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* coords, int64_t k0, const float* fsrc,
+                                int m_or_D, int d_begin, int Dc, int T, const GridParams* gp, const double* G,
+                                const GradOut& gout, cudaStream_t st, int num_sms);
 wect_status launch_finalize(const void* diff, bool is_float, int64_t rows, int T, void* out, wect_dtype odtype,
                             cudaStream_t st);
 
@@ -489,6 +492,110 @@ static wect_status run_complex(int mode, const wect_complex_desc* K, const float
   s = launch_finalize(diff, floatw, Dc, T, ov.dev, odtype, st);
   if (s != WECT_OK) return s;
   return out_finish(ov, st);
+}
+
+// ------------------------------------------------ backward (weights gradient)
+
+static wect_status run_complex_grad(int mode, const wect_complex_desc* K, const float* fsrc, int32_t D,
+                                    const wect_grid* grid, const double* G, double* grad_vweights,
+                                    double* const* grad_cells, void* stream) {
+  g_msg[0] = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  wect_status s = validate_complex(K, mode == 0);
+  if (s != WECT_OK) return s;
+  if (!grid) return fail(WECT_EINVAL, "grid is NULL");
+  TimeScope ts(grid->flags);
+  if (grid->T < 2) return fail(WECT_EINVAL, "T must be >= 2 (beta divides by T-1)");
+  if (grid->T > 4096) return fail(WECT_ENOTSUP, "T > 4096 not supported");
+  if (D < 1) return fail(WECT_EINVAL, mode == 0 ? "need D >= 1 directions" : "need m >= 1 filters");
+  if (!fsrc && K->k0 > 0) return fail(WECT_EINVAL, mode == 0 ? "dirs is NULL" : "fvals is NULL");
+  int d_begin, Dc;
+  s = resolve_rows(grid, D, &d_begin, &Dc);
+  if (s != WECT_OK) return s;
+  if (!G && Dc > 0 && K->k0 > 0) return fail(WECT_EINVAL, "G is NULL");
+  const int T = grid->T;
+  const int n = K->n;
+  const int nsm = num_sms_current();
+  Arena ar(st);
+  // outputs (device views; host outputs are copied back at the end)
+  GradOut gout;
+  memset(&gout, 0, sizeof(gout));
+  std::vector<OutView> views;
+  Segs segs;
+  memset(&segs, 0, sizeof(segs));
+  segs.s[0].count = K->k0;
+  segs.s[0].arity = 1;
+  segs.s[0].sign = 1;
+  if (grad_vweights) {
+    views.push_back(out_view(ar, grad_vweights, (size_t)K->k0 * 8));
+    gout.g[0] = (double*)views.back().dev;
+  }
+  int ns = 1;
+  int64_t total = K->k0;
+  for (int i = 0; i < K->ncell_dims; ++i) {
+    const wect_cells& c = K->cells[i];
+    if (c.count == 0) continue;
+    Seg& g = segs.s[ns];
+    g.verts = (const int32_t*)ar.in(c.verts, (size_t)c.count * c.arity * 4);
+    g.count = c.count;
+    g.start = total;
+    g.arity = c.arity;
+    g.sign = (c.dim % 2 == 0) ? 1 : -1;
+    total += c.count;
+    if (grad_cells && grad_cells[i]) {
+      views.push_back(out_view(ar, grad_cells[i], (size_t)c.count * 8));
+      gout.g[ns] = (double*)views.back().dev;
+    }
+    ++ns;
+  }
+  for (int i = ns; i < kMaxSegs; ++i) { segs.s[i].start = total; segs.s[i].count = (int64_t)1 << 62; }
+  segs.nseg = ns;
+  segs.total = total;
+  if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging", __FILE__, __LINE__);
+  if (K->k0 == 0) return WECT_OK;
+  if (Dc == 0) {  // no rows: the gradient is 0
+    for (auto& v : views) WECT_CUDA_TRY(cudaMemsetAsync(v.dev, 0, v.bytes, st));
+    for (auto& v : views) { s = out_finish(v, st); if (s != WECT_OK) return s; }
+    return WECT_OK;
+  }
+  const float* coords = mode == 0 ? (const float*)ar.in(K->coords, (size_t)K->k0 * n * 4) : nullptr;
+  const float* dsrc = mode == 0 ? (const float*)ar.in(fsrc, (size_t)D * n * 4)
+                                : (const float*)ar.in(fsrc, (size_t)K->k0 * D * 4);
+  const double* dG = (const double*)ar.in(G, (size_t)Dc * T * 8);
+  unsigned long long* words = (unsigned long long*)ar.alloc(64);
+  GridParams* gp = (GridParams*)ar.alloc(sizeof(GridParams));
+  if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging/scratch", __FILE__, __LINE__);
+  unsigned long long* m64 = words;
+  unsigned int* w32 = (unsigned int*)(words + 1);
+  unsigned int *m32 = w32, *r1 = w32 + 1, *smax = w32 + 2;
+  WECT_CUDA_TRY(cudaMemsetAsync(words, 0, 64, st));
+  if (mode == 0) {
+    float* vmax = (float*)ar.alloc((size_t)K->k0 * 4);
+    if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
+    s = launch_vmax(n, coords, K->k0, dsrc, D, vmax, m32, r1, smax, m64, st, nsm);
+  } else {
+    s = launch_absmax_f32(dsrc, K->k0 * (int64_t)D, m32, st, nsm);
+  }
+  if (s != WECT_OK) return s;
+  s = launch_complex_params(mode, n, m64, m32, r1, smax, *grid, gp, st);
+  if (s != WECT_OK) return s;
+  s = launch_complex_grad(mode, n, segs, coords, K->k0, dsrc, D, d_begin, Dc, T, gp, dG, gout, st, nsm);
+  if (s != WECT_OK) return s;
+  for (auto& v : views) {
+    s = out_finish(v, st);
+    if (s != WECT_OK) return s;
+  }
+  return WECT_OK;
+}
+
+wect_status wect_complex_backward(const wect_complex_desc* K, const float* dirs, int32_t D, const wect_grid* grid,
+                                  const double* G, double* grad_vweights, double* const* grad_cells, void* stream) {
+  return run_complex_grad(0, K, dirs, D, grid, G, grad_vweights, grad_cells, stream);
+}
+
+wect_status ecf_complex_backward(const wect_complex_desc* K, const float* fvals, int32_t m, const wect_grid* grid,
+                                 const double* G, double* grad_vweights, double* const* grad_cells, void* stream) {
+  return run_complex_grad(1, K, fvals, m, grid, G, grad_vweights, grad_cells, stream);
 }
 
 wect_status wect_complex(const wect_complex_desc* K, const float* dirs, int32_t D, const wect_grid* grid, void* out,

@@ -43,6 +43,11 @@ struct Segs {
   int64_t total;
 };
 
+// Backward outputs (k_grad.cu): per segment an [count] fp64 gradient, or nullptr (skip).
+struct GradOut {
+  double* g[kMaxSegs];
+};
+
 // Device-global diagnostics (one per device, per loaded library).
 extern __device__ unsigned int g_err_word;            // bit 0: out-of-range vertex index
 extern __device__ unsigned long long g_repair_count;  // binary64 near-edge repairs

@@ -1,0 +1,187 @@
+// k_grad.cu -- gradient of a scalar loss through the WECT / WECFs with respect to the
+// weights (wect_complex_backward, ecf_complex_backward).
+//
+// The paper's framework is differentiable with respect to the weights (P:114-115,
+// P:493-494).  Alg. 1 is linear in the weights:
+//   out[p, q] = sum over cells s of w(s) (-1)^dim s [bin(s, p) <= q]     (closed form P:769-776)
+// so for G = dL/dout,
+//   dL/dw(s) = (-1)^dim s * sum_p RC[p, bin(s, p)],   RC[p, q] = sum_{q' >= q} G[p, q'].
+// (Heights / coordinates enter only through the piecewise-constant bins: gradient 0 a.e.)
+//
+// Passes: k_rcumsum (RC, one thread per row, q from T-1 down); per tile of 64 filters the
+// exact vertex-bin table VB (k_vbins of the forward for directions, k_vbins_f here for
+// given filter values); then k_grad_cells twice per tile (32 filters each, one per lane):
+// a warp takes 32 cells, the cell bin per lane is the max of its vertices' VB entries
+// (eq. msi, exact because alpha is monotone), each lane gathers RC[bin] from a
+// shared-memory tile, and a 31-shuffle transpose-reduction leaves lane c with cell c's
+// sum over the 32 filters.  Tiles add into the fp64 gradient in a fixed order, so the
+// result is deterministic.
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace wect {
+
+constexpr int kGradWarps = 8;
+
+
+__global__ void k_rcumsum(const double* __restrict__ G, int64_t rows, int T, double* __restrict__ RC) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double acc = 0.0;
+  for (int q = T - 1; q >= 0; --q) {
+    acc = __dadd_rn(acc, G[r * T + q]);
+    RC[r * T + q] = acc;
+  }
+}
+
+// VB rows for given filter values (ECF): VB[v] word l = alpha(f[v, p0+2l]) | alpha(f[v, p0+2l+1]) << 16,
+// alpha in binary64 on the fp32 value (reading A1; no fast path needed here).
+__global__ void __launch_bounds__(256) k_vbins_f(const float* __restrict__ f, int64_t k0, int m, int p0, int np,
+                                                 const GridParams* __restrict__ gp, uint32_t* __restrict__ vb) {
+  const GridParams g = *gp;
+  const int lane = threadIdx.x & 31;
+  const int pa = 2 * lane, pb = 2 * lane + 1;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < k0; v += nwarps) {
+    const int ba = pa < np ? alpha64((double)__ldg(f + v * m + p0 + pa), g) : 0;
+    const int bb = pb < np ? alpha64((double)__ldg(f + v * m + p0 + pb), g) : 0;
+    vb[v * 32 + lane] = (uint32_t)ba | ((uint32_t)bb << 16);
+  }
+}
+
+// lane c of the warp ends with sum over lanes of v[c] (31 shuffles, recursive halving)
+__device__ __forceinline__ double transpose_reduce(double (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = up ? v[k] : v[k + o];
+      const double keep = up ? v[k + o] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
+
+// One pass: filters [row0, row0 + np) of the tile (np <= 32), lane = filter.
+// vb: the tile's VB table (u16 column (half * 32 + lane) of each 64-filter row).
+template <bool SMEM_RC>
+__global__ void __launch_bounds__(kGradWarps * 32) k_grad_cells(Segs segs, int64_t k0, const uint32_t* __restrict__ vb,
+                                                                int half, int np, const double* __restrict__ RC,
+                                                                int row0, int T, GradOut gout, int first) {
+  extern __shared__ __align__(16) double rcs[];  // [T][32]
+  const int lane = threadIdx.x & 31;
+  if (SMEM_RC) {
+    for (int i = threadIdx.x; i < T * 32; i += blockDim.x) {
+      const int q = i >> 5, l = i & 31;
+      rcs[i] = l < np ? RC[(int64_t)(row0 + l) * T + q] : 0.0;
+    }
+    __syncthreads();
+  }
+  const uint16_t* vb16 = (const uint16_t*)vb + half * 32 + lane;
+  const int64_t gw = (int64_t)blockIdx.x * kGradWarps + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kGradWarps;
+  for (int si = 0; si < segs.nseg; ++si) {
+    const Seg S = segs.s[si];
+    double* go = gout.g[si];
+    if (!go || S.count == 0) continue;
+    const int ar = S.arity;
+    for (int64_t base = gw * 32; base < S.count; base += nwarps * 32) {
+      const int64_t mycell = base + lane;
+      int ids[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int id = 0;
+        if (j < ar && mycell < S.count) {
+          id = S.verts ? __ldg(S.verts + mycell * ar + j) : (int)mycell;
+          if ((unsigned)id >= (unsigned)k0) {
+            atomicOr(&g_err_word, 1u);
+            id = -1;
+          }
+        }
+        ids[j] = id;
+      }
+      double v[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        int bin = 0;
+        bool ok = true;
+        for (int j = 0; j < ar; ++j) {
+          const int id = __shfl_sync(0xffffffffu, ids[j], c);
+          ok &= id >= 0;
+          bin = max(bin, (int)__ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64));
+        }
+        double x = 0.0;
+        if (ok && lane < np) x = SMEM_RC ? rcs[bin * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bin);
+        v[c] = x;
+      }
+      const double sum = transpose_reduce(v, lane);
+      if (mycell < S.count) {
+        const double gcell = S.sign < 0 ? -sum : sum;
+        go[mycell] = first ? gcell : go[mycell] + gcell;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+wect_status launch_vbins_tile(int n, const float* coords, int64_t k0, const float* dirs, int p0, int np,
+                              const GridParams* gp, uint32_t* vb, cudaStream_t st, int num_sms);
+
+wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* coords, int64_t k0, const float* fsrc,
+                                int m_or_D, int d_begin, int Dc, int T, const GridParams* gp, const double* G,
+                                const GradOut& gout, cudaStream_t st, int num_sms) {
+  for (int i = 0; i < segs.nseg; ++i)
+    if (segs.s[i].arity > 8) return fail(WECT_ENOTSUP, "backward supports cells of arity <= 8");
+  double* RC = nullptr;
+  uint32_t* vb = nullptr;
+  WECT_CUDA_TRY(cudaMallocAsync((void**)&RC, (size_t)Dc * T * sizeof(double), st));
+  WECT_CUDA_TRY(cudaMallocAsync((void**)&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t), st));
+  k_rcumsum<<<(unsigned)((Dc + 127) / 128), 128, 0, st>>>(G, Dc, T, RC); count_launch();
+  WECT_CUDA_TRY(cudaGetLastError());
+  const size_t smem = (size_t)T * 32 * sizeof(double);
+  const bool use_smem = smem <= 160 * 1024;
+  if (use_smem) {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_grad_cells<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  int64_t maxc = 0;
+  for (int i = 0; i < segs.nseg; ++i) maxc = segs.s[i].count > maxc ? segs.s[i].count : maxc;
+  int64_t want = (maxc + 32 * kGradWarps - 1) / (32 * kGradWarps);
+  const int per_sm = use_smem ? (int)((200 * 1024) / smem > 4 ? 4 : ((200 * 1024) / smem < 1 ? 1 : (200 * 1024) / smem)) : 4;
+  const int ctas = (int)(want < (int64_t)num_sms * per_sm ? (want < 1 ? 1 : want) : (int64_t)num_sms * per_sm);
+  wect_status s = WECT_OK;
+  for (int t0 = 0; t0 < Dc && s == WECT_OK; t0 += 64) {
+    const int np = (Dc - t0) < 64 ? (Dc - t0) : 64;
+    if (mode == 0) {
+      s = launch_vbins_tile(n, coords, k0, fsrc, d_begin + t0, np, gp, vb, st, num_sms);
+      if (s != WECT_OK) break;
+    } else {
+      int vblocks = (int)((k0 + 7) / 8);
+      vblocks = vblocks > num_sms * 16 ? num_sms * 16 : (vblocks < 1 ? 1 : vblocks);
+      k_vbins_f<<<vblocks, 256, 0, st>>>(fsrc, k0, m_or_D, d_begin + t0, np, gp, vb); count_launch();
+    }
+    for (int half = 0; half < 2; ++half) {
+      const int nph = np - 32 * half;
+      if (nph <= 0) break;
+      const int first = (t0 == 0 && half == 0) ? 1 : 0;
+      MainTimer timer(st);
+      if (use_smem)
+        k_grad_cells<true><<<ctas, kGradWarps * 32, smem, st>>>(segs, k0, vb, half, nph < 32 ? nph : 32, RC,
+                                                               t0 + 32 * half, T, gout, first);
+      else
+        k_grad_cells<false><<<ctas, kGradWarps * 32, 0, st>>>(segs, k0, vb, half, nph < 32 ? nph : 32, RC,
+                                                             t0 + 32 * half, T, gout, first);
+      count_launch();
+      timer.stop();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) s = fail_cuda(e, "k_grad_cells", __FILE__, __LINE__);
+    }
+  }
+  cudaFreeAsync(RC, st);
+  cudaFreeAsync(vb, st);
+  return s;
+}
+
+}  // namespace wect

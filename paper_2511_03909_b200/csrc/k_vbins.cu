@@ -561,4 +561,21 @@ wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float*
   return fail(WECT_EINVAL, "ambient dimension n=%d outside [1,8]", n);
 }
 
+// one tile of the vertex-bin table (also used by the backward pass, k_grad.cu)
+wect_status launch_vbins_tile(int n, const float* coords, int64_t k0, const float* dirs, int p0, int np,
+                              const GridParams* gp, uint32_t* vb, cudaStream_t st, int num_sms) {
+  int vblocks = (int)((k0 + 255) / 256);
+  vblocks = vblocks > num_sms * 8 ? num_sms * 8 : (vblocks < 1 ? 1 : vblocks);
+  switch (n) {
+#define WECT_CASE(NN) \
+  case NN: k_vbins<NN><<<vblocks, 256, 0, st>>>(coords, k0, dirs, p0, np, gp, vb); break;
+    WECT_CASE(1) WECT_CASE(2) WECT_CASE(3) WECT_CASE(4) WECT_CASE(5) WECT_CASE(6) WECT_CASE(7) WECT_CASE(8)
+#undef WECT_CASE
+    default: return fail(WECT_EINVAL, "ambient dimension n=%d outside [1,8]", n);
+  }
+  count_launch();
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
 }  // namespace wect

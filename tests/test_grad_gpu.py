@@ -1,0 +1,107 @@
+"""GPU parity of wect_complex_backward / ecf_complex_backward against
+the oracle's closed-form gradient (oracle.wecfs_grad).  Integer-valued G: every partial sum
+is an exact binary64 integer, so the comparison is bit-exact.  Random fp64 G: reading A13,
+|gpu - oracle| <= 1e-12 * sum|G| of the rows (binary64 reassociation only)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2511_03909_b200 as w  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _cells(cx):
+    return [(torch.from_numpy(np.ascontiguousarray(c.verts, np.int32)).to(DEV), None, c.dim) for c in cx.cells]
+
+
+def _check(gv, gc, ov, oc, G, exact):
+    tol = 0.0 if exact else 1e-12 * float(np.abs(G).sum())
+    assert np.abs(gv.cpu().numpy() - ov).max(initial=0.0) <= tol
+    for a, b in zip(gc, oc):
+        assert np.abs(a.cpu().numpy() - b).max(initial=0.0) <= tol
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("exact", [True, False])
+def test_wect_backward_vs_oracle(seed, exact):
+    rng = np.random.default_rng(6000 + seed)
+    n = [2, 3, 3, 4, 5, 3][seed]
+    cx = synth.random_small_complex(seed, n=n, nverts=60 + 20 * seed, ntop=50, kmax=min(3, n))
+    D, T = [(1, 7), (9, 64), (70, 33), (64, 512), (33, 2), (130, 128)][seed]
+    dirs = synth.directions_s1(D) if n == 2 else synth.directions_sphere(D, n, 6100 + seed)
+    G = rng.integers(-5, 6, size=(D, T)).astype(np.float64) if exact else rng.standard_normal((D, T))
+    gv, gc = w.wect_complex_backward(torch.from_numpy(cx.coords).to(DEV), _cells(cx), torch.from_numpy(dirs).to(DEV),
+                                     T, torch.from_numpy(G).to(DEV))
+    w.sync_status()
+    ov, oc = oracle.wect_complex_grad(cx, dirs, T, G)
+    _check(gv, gc, ov, oc, G, exact)
+
+
+def test_wect_backward_row_slice_and_host_buffers():
+    cx = synth.torus_mesh(9, 11, 3)
+    dirs = synth.directions_sphere(100, 3, 6200)
+    T = 40
+    G = np.random.default_rng(1).integers(-4, 5, size=(100, T)).astype(np.float64)
+    ov, oc = oracle.wect_complex_grad(cx, dirs, T, G)
+    # host (numpy) buffers: the library stages them
+    gv, gc = w.wect_complex_backward(cx.coords, [(c.verts, None, c.dim) for c in cx.cells], dirs, T, G)
+    _check(gv, gc, ov, oc, G, True)
+    # rows 30..79 only: the gradient of L restricted to those rows, with M over ALL rows (A2)
+    ov2, oc2 = oracle.wecfs_grad(oracle.heights(cx.coords, dirs)[:, 30:80], cx, T,
+                                 -oracle.maxheight(oracle.heights(cx.coords, dirs)),
+                                 oracle.maxheight(oracle.heights(cx.coords, dirs)), G[30:80])
+    gv2, gc2 = w.wect_complex_backward(cx.coords, [(c.verts, None, c.dim) for c in cx.cells], dirs, T,
+                                       np.ascontiguousarray(G[30:80]), d_begin=30, d_count=50)
+    _check(gv2, gc2, ov2, oc2, G, True)
+
+
+@pytest.mark.parametrize("m,T", [(1, 512), (5, 17), (77, 256)])
+def test_ecf_backward_vs_oracle(m, T):
+    cx = synth.torus_mesh(12, 10, m)
+    f = np.random.default_rng(m).uniform(-1, 1, (cx.k0, m)).astype(np.float32)
+    G = np.random.default_rng(m + 1).integers(-3, 4, size=(m, T)).astype(np.float64)
+    gv, gc = w.ecf_complex_backward(torch.from_numpy(f).to(DEV), _cells(cx), T, torch.from_numpy(G).to(DEV))
+    ov, oc = oracle.ecf_complex_grad(cx, f, T, G)
+    _check(gv, gc, ov, oc, G, True)
+    gv, gc = w.ecf_complex_backward(torch.from_numpy(f).to(DEV), _cells(cx), T, torch.from_numpy(G).to(DEV),
+                                    lo=-2.0, hi=0.5)
+    ov, oc = oracle.ecf_complex_grad(cx, f, T, G, -2.0, 0.5)
+    _check(gv, gc, ov, oc, G, True)
+
+
+def test_backward_large_T_global_rc_path():
+    cx = synth.torus_mesh(8, 9, 4)
+    dirs = synth.directions_sphere(40, 3, 6300)
+    T = 1000  # RC tile > 160 KB: gathered from global memory
+    G = np.random.default_rng(2).integers(-3, 4, size=(40, T)).astype(np.float64)
+    gv, gc = w.wect_complex_backward(cx.coords, [(c.verts, None, c.dim) for c in cx.cells], dirs, T, G)
+    ov, oc = oracle.wect_complex_grad(cx, dirs, T, G)
+    _check(gv, gc, ov, oc, G, True)
+
+
+def test_backward_mesh_euler_identity_at_scale():
+    """cfg4-shaped mesh (scaled): L(w) from the GPU forward equals sum w * grad from the GPU
+    backward, exactly (integer weights, integer G)."""
+    c = synth.make_config(3, scale=0.02)
+    cx, dirs = c["complex"], c["dirs"][:96]
+    T = 512
+    G = np.random.default_rng(3).integers(-2, 3, size=(96, T)).astype(np.float64)
+    cells = [(torch.from_numpy(x.verts).to(DEV), torch.from_numpy(x.weights).to(DEV), x.dim) for x in cx.cells]
+    fwd = w.wect_complex(torch.from_numpy(cx.coords).to(DEV), cells, torch.from_numpy(dirs).to(DEV), T,
+                         vweights=torch.from_numpy(cx.vweights).to(DEV)).cpu().numpy()
+    L = float((fwd.astype(np.float64) * G).sum())
+    gv, gc = w.wect_complex_backward(torch.from_numpy(cx.coords).to(DEV), cells, torch.from_numpy(dirs).to(DEV), T,
+                                     torch.from_numpy(G).to(DEV))
+    lin = float((cx.vweights.astype(np.float64) * gv.cpu().numpy()).sum())
+    for x, g in zip(cx.cells, gc):
+        lin += float((x.weights.astype(np.float64) * g.cpu().numpy()).sum())
+    assert lin == L
