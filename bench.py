@@ -9,7 +9,7 @@ wect_images call over the batch = every row of SURVEY.md section 8(a): grid M
 kernel (a0, a4-a7: implicit cells, max rule, signed regrouped accumulation,
 cumsum, 1.97 GB output write).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx|ecfimg|ecfimg1k] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx|ecfimg|ecfimg1k|bwd3|bwd4] [--impl reference]
 
 Multi-GPU (torchrun, one rank per GPU): images are sharded by batch with no data-path
 collective (weak scaling: every rank runs its own 60,000-image shard); times are the
@@ -150,6 +150,19 @@ def workload(cfg: str, rank: int):
                     alg_bytes=B * nv + B * T * 4, unit="complexes/s",
                     desc=f"image ECF: {B}x{'x'.join(map(str, dims))} u8 ({kind}), intensity filter, grid [0, 255], "
                          f"T={T}, int32 out")
+    if cfg in ("bwd3", "bwd4"):
+        # weights gradient through the WECT on the cfg4 / cfg5 complex
+        c = 3 if cfg == "bwd3" else 4
+        d = synth.make_config(c)
+        cx, dirs, T = d["complex"], d["dirs"], d["T"]
+        ncells = cx.num_cells()
+        D = dirs.shape[0]
+        G = synth.rng(synth.S0 + 70 + c).integers(-3, 4, size=(D, T)).astype(np.float64)
+        idx_bytes = sum(c_.verts.nbytes for c_ in cx.cells)
+        return dict(kind="grad", name=d["name"] + "_backward", cx=cx, dirs=dirs, T=T, G=G, units=1,
+                    updates=ncells * D, atomics=ncells * D,
+                    alg_bytes=cx.coords.nbytes + idx_bytes + G.nbytes + ncells * 8, unit="complexes/s",
+                    desc=f"dL/dweights through the WECT of {cx.k0} V / {ncells} cells, n={cx.n}, D={D}, T={T}")
     if cfg in ("3", "4", "ecfx"):
         c = 3 if cfg in ("3", "ecfx") else 4
         d = synth.make_config(c)
@@ -208,7 +221,15 @@ def run_ours(args, rank, world, local_rank):
         cells = [(torch.from_numpy(c.verts).to(dev), None if c.weights is None else torch.from_numpy(c.weights).to(dev),
                   c.dim) for c in cx.cells]
         vw = None if cx.vweights is None else torch.from_numpy(cx.vweights).to(dev)
-        if wl["kind"] == "ecf":
+        if wl["kind"] == "grad":
+            coords_d = torch.from_numpy(cx.coords).to(dev)
+            dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
+            G_d = torch.from_numpy(wl["G"]).to(dev)
+            out_d = G_d
+
+            def step(flags=0):
+                w.wect_complex_backward(coords_d, cells, dirs_d, wl["T"], G_d, flags=flags)
+        elif wl["kind"] == "ecf":
             f_d = torch.from_numpy(wl["fvals"]).to(dev)
             out_d = torch.empty((1, wl["T"]), dtype=torch.float64 if cx.is_float else torch.int64, device=dev)
 
@@ -272,6 +293,8 @@ def run_ours(args, rank, world, local_rank):
         kname, bound = "k_sweep2d", "hbm"
     elif wl["kind"] == "images":
         kname, bound = "k_grid_hist", "alu"
+    elif wl["kind"] == "grad":
+        kname, bound = "k_grad_cells", "alu"
     elif wl["kind"] == "ecf" or D <= 8:
         kname, bound = "k_stream", "hbm"
     else:
@@ -305,7 +328,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "int32" if wl.get("out_dtype") == "int32" else ("f64" if "cx" in wl and wl["cx"].is_float else "int64"),
+        "dtype": "int32" if wl.get("out_dtype") == "int32" else ("f64" if wl["kind"] == "grad" or ("cx" in wl and wl["cx"].is_float) else "int64"),
         "data": "synthetic (seeded; DESIGN.md input recipe)",
         "config": {"workload": wl["name"], "desc": wl["desc"], "per_gpu_units": wl["units"],
                    "l2": f"flushed between timed steps ({flush.numel() >> 20} MiB write, untimed)",
@@ -360,6 +383,17 @@ def run_ours(args, rank, world, local_rank):
                       "h2d_bytes_per_step": int(img_h.numel() + dirs_h.numel() * 4),
                       "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()), "steps": ke,
                       "path": "wect_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"}
+    elif not args.no_e2e and wl["kind"] == "grad":
+        cx = wl["cx"]
+        cells_h = [(c.verts, None, c.dim) for c in cx.cells]
+        t0 = time.perf_counter()
+        ke = 2
+        for _ in range(ke):
+            gv, gc = w.wect_complex_backward(cx.coords, cells_h, wl["dirs"], wl["T"], wl["G"])
+        e2e_s = time.perf_counter() - t0
+        res["e2e"] = {"value": world * ke / e2e_s, "unit": wl["unit"],
+                      "h2d_bytes_per_step": int(cx.coords.nbytes + sum(c.verts.nbytes for c in cx.cells) + wl["G"].nbytes),
+                      "d2h_bytes_per_step": int(8 * (gv.numel() + sum(g.numel() for g in gc))), "steps": ke}
     elif not args.no_e2e:
         cx = wl["cx"]
         cells_h = [(c.verts, c.weights, c.dim) for c in cx.cells]
@@ -430,6 +464,24 @@ def cpu_baseline(wl, budget_s=15.0, max_units=None):
     import oracle as orc
 
     cx = wl["cx"]
+    if wl["kind"] == "grad":
+        # the closed-form oracle gradient on a bounded sample: 2 directions, full complex
+        import synth as sy
+
+        nd, per_dim = 2, 4000
+        sub = sy.Complex(cx.coords, cx.vweights, [sy.Cells(c.verts[:per_dim], None, c.dim) for c in cx.cells],
+                         cx.k0, is_float=False)
+        sampled = cx.k0 + sum(min(per_dim, len(c.verts)) for c in cx.cells)
+        t0 = time.perf_counter()
+        fv = orc.heights(cx.coords, wl["dirs"][:nd])
+        M = orc.maxheight(fv)
+        orc.wecfs_grad(fv, sub, wl["T"], -M, M, wl["G"][:nd])
+        t = time.perf_counter() - t0
+        D = wl["dirs"].shape[0]
+        scale = (D / nd) * (cx.num_cells() / sampled)
+        return {"value": 1.0 / (t * scale), "unit": wl["unit"], "cores": 1, "kind": "oracle",
+                "sample": f"closed-form gradient oracle on {nd} of {D} directions, all vertices + the first "
+                          f"{per_dim} cells of each dimension ({t:.1f} s), scaled by D/{nd} x cells/sampled"}
     if wl["kind"] == "ecf":
         t0 = time.perf_counter()
         orc.ecf_complex(cx, wl["fvals"], wl["T"])
@@ -491,7 +543,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4), ecfx, ecfimg or ecfimg1k")
+    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4), ecfx, ecfimg, ecfimg1k, bwd3 or bwd4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

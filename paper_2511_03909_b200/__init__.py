@@ -206,7 +206,7 @@ def ecf_complex(fvals, cells: Sequence[Tuple], T: int, *, vweights=None, is_floa
                         _device_of(fvals, vweights, *[c[0] for c in cells]))
 
 
-def _run_backward(fn, k0, n, coords, cells, src, D, T, G, d_begin, d_count, maxheight, lo, hi, stream, dev_hint):
+def _run_backward(fn, k0, n, coords, cells, src, D, T, G, d_begin, d_count, maxheight, lo, hi, flags, stream, dev_hint):
     L = _lib.load()
     arr, keep = _cells_array([(v, None, d) for v, _, d in cells], False)
     desc = _lib.wect_complex_desc(_ptr(coords), int(k0), int(n), None, arr, len(cells), _lib.I32)
@@ -215,32 +215,32 @@ def _run_backward(fn, k0, n, coords, cells, src, D, T, G, d_begin, d_count, maxh
     gv = _alloc_out((int(k0),), "float64", dev, None)
     gc = [_alloc_out((int(v.shape[0]),), "float64", dev, None) for v, _, _ in cells]
     ptrs = (ctypes.c_void_p * max(1, len(cells)))(*[_ptr(x) for x in gc])
-    g = _grid(T, d_begin, d_count, maxheight, lo, hi, 0)
+    g = _grid(T, d_begin, d_count, maxheight, lo, hi, flags)
     _lib.check(fn(ctypes.byref(desc), _ptr(src), int(D), ctypes.byref(g), _ptr(G), _ptr(gv), ptrs, _stream(dev, stream)))
     del keep
     return gv, gc
 
 
 def wect_complex_backward(coords, cells: Sequence[Tuple], dirs, T: int, G, *, d_begin: int = 0, d_count: int = 0,
-                          maxheight: float = 0.0, stream=None):
+                          maxheight: float = 0.0, flags: int = 0, stream=None):
     """dL/dweights through wect_complex for G = dL/dout [rows, T] (fp64).  Returns
     (grad_vweights [k0], [grad_cells_i [count_i]]) in float64 (include/wect.h)."""
     coords = _as(coords, np.float32, "float32")
     dirs = _as(dirs, np.float32, "float32")
     k0, n = int(coords.shape[0]), int(coords.shape[1])
     return _run_backward(_lib.load().wect_complex_backward, k0, n, coords, cells, dirs, int(dirs.shape[0]), T, G,
-                         d_begin, d_count, maxheight, 0.0, 0.0, stream, _device_of(coords, dirs, G))
+                         d_begin, d_count, maxheight, 0.0, 0.0, flags, stream, _device_of(coords, dirs, G))
 
 
 def ecf_complex_backward(fvals, cells: Sequence[Tuple], T: int, G, *, d_begin: int = 0, d_count: int = 0,
-                         maxheight: float = 0.0, lo: float = 0.0, hi: float = 0.0, stream=None):
+                         maxheight: float = 0.0, lo: float = 0.0, hi: float = 0.0, flags: int = 0, stream=None):
     """dL/dweights through ecf_complex for G = dL/dout [rows, T] (fp64)."""
     fvals = _as(fvals, np.float32, "float32")
     if fvals.ndim == 1:
         fvals = fvals.reshape(-1, 1)
     k0, m = int(fvals.shape[0]), int(fvals.shape[1])
     return _run_backward(_lib.load().ecf_complex_backward, k0, 1, None, cells, fvals, m, T, G, d_begin, d_count,
-                         maxheight, lo, hi, stream, _device_of(fvals, G))
+                         maxheight, lo, hi, flags, stream, _device_of(fvals, G))
 
 
 def wect_maxheight(coords, dirs, stream=None) -> float:

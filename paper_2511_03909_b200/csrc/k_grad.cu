@@ -65,8 +65,77 @@ __device__ __forceinline__ double transpose_reduce(double (&v)[32], int lane) {
   return v[0];
 }
 
+// Bins of cells base + c, c < 32, for this lane's filter, 8 cells at a time with all
+// 8 * AR row loads in flight before the max (AR > 0: compile-time arity).
+template <int AR>
+__device__ __forceinline__ void cell_bins(const int (&ids)[8], int ar, const uint16_t* __restrict__ vb16,
+                                          int (&bins)[32], uint32_t& okmask) {
+  okmask = 0xffffffffu;
+#pragma unroll
+  for (int c0 = 0; c0 < 32; c0 += 8) {
+    int b[8][AR > 0 ? AR : 8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+#pragma unroll
+      for (int j = 0; j < (AR > 0 ? AR : 8); ++j) {
+        if (AR == 0 && j >= ar) { b[c][j] = 0; continue; }
+        const int id = __shfl_sync(0xffffffffu, ids[j], c0 + c);
+        if (id < 0) okmask &= ~(1u << (c0 + c));
+        b[c][j] = __ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      int m = b[c][0];
+#pragma unroll
+      for (int j = 1; j < (AR > 0 ? AR : 8); ++j) m = max(m, b[c][j]);
+      bins[c0 + c] = m;
+    }
+  }
+}
+
 // One pass: filters [row0, row0 + np) of the tile (np <= 32), lane = filter.
 // vb: the tile's VB table (u16 column (half * 32 + lane) of each 64-filter row).
+template <bool SMEM_RC, int AR>
+__device__ __forceinline__ void grad_segment(const Seg& S, double* __restrict__ go, int64_t k0,
+                                             const uint16_t* __restrict__ vb16, int np, const double* __restrict__ rcs,
+                                             const double* __restrict__ RC, int row0, int T, int first, int64_t gw,
+                                             int64_t nwarps, int lane) {
+  const int ar = AR > 0 ? AR : S.arity;
+  for (int64_t base = gw * 32; base < S.count; base += nwarps * 32) {
+    const int64_t mycell = base + lane;
+    int ids[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int id = 0;
+      if (j < ar && mycell < S.count) {
+        id = S.verts ? __ldg(S.verts + mycell * ar + j) : (int)mycell;
+        if ((unsigned)id >= (unsigned)k0) {
+          atomicOr(&g_err_word, 1u);
+          id = -1;
+        }
+      }
+      ids[j] = id;
+    }
+    int bins[32];
+    uint32_t okmask;
+    cell_bins<AR>(ids, ar, vb16, bins, okmask);
+    double v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      double x = 0.0;
+      if (((okmask >> c) & 1u) && lane < np)
+        x = SMEM_RC ? rcs[bins[c] * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bins[c]);
+      v[c] = x;
+    }
+    const double sum = transpose_reduce(v, lane);
+    if (mycell < S.count) {
+      const double gcell = S.sign < 0 ? -sum : sum;
+      go[mycell] = first ? gcell : go[mycell] + gcell;
+    }
+  }
+}
+
 template <bool SMEM_RC>
 __global__ void __launch_bounds__(kGradWarps * 32) k_grad_cells(Segs segs, int64_t k0, const uint32_t* __restrict__ vb,
                                                                 int half, int np, const double* __restrict__ RC,
@@ -87,41 +156,12 @@ __global__ void __launch_bounds__(kGradWarps * 32) k_grad_cells(Segs segs, int64
     const Seg S = segs.s[si];
     double* go = gout.g[si];
     if (!go || S.count == 0) continue;
-    const int ar = S.arity;
-    for (int64_t base = gw * 32; base < S.count; base += nwarps * 32) {
-      const int64_t mycell = base + lane;
-      int ids[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        int id = 0;
-        if (j < ar && mycell < S.count) {
-          id = S.verts ? __ldg(S.verts + mycell * ar + j) : (int)mycell;
-          if ((unsigned)id >= (unsigned)k0) {
-            atomicOr(&g_err_word, 1u);
-            id = -1;
-          }
-        }
-        ids[j] = id;
-      }
-      double v[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        int bin = 0;
-        bool ok = true;
-        for (int j = 0; j < ar; ++j) {
-          const int id = __shfl_sync(0xffffffffu, ids[j], c);
-          ok &= id >= 0;
-          bin = max(bin, (int)__ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64));
-        }
-        double x = 0.0;
-        if (ok && lane < np) x = SMEM_RC ? rcs[bin * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bin);
-        v[c] = x;
-      }
-      const double sum = transpose_reduce(v, lane);
-      if (mycell < S.count) {
-        const double gcell = S.sign < 0 ? -sum : sum;
-        go[mycell] = first ? gcell : go[mycell] + gcell;
-      }
+    switch (S.arity) {
+      case 1: grad_segment<SMEM_RC, 1>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 2: grad_segment<SMEM_RC, 2>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 3: grad_segment<SMEM_RC, 3>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 4: grad_segment<SMEM_RC, 4>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      default: grad_segment<SMEM_RC, 0>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
     }
   }
 }
