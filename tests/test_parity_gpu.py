@@ -442,3 +442,36 @@ def test_high_arity_cells_take_the_generic_kernel():
         cx = synth.random_small_complex(seed, n=3, nverts=60, ntop=12, kmax=kmax)
         dirs = synth.directions_sphere(40, 3, seed)
         assert (gpu_wect_complex(cx, dirs, 97) == oracle.wect_complex(cx, dirs, 97)).all()
+
+
+def test_ecf_single_filter_integer_weights_vs_O2():
+    """ecf_complex with m = 1 and integer weights (the ECF-X shape): arities 2..8, ragged
+    segment tails, unit weights, |w| ~ 2^30 (int64 direct adds), a misaligned list, both
+    grids."""
+    g = np.random.default_rng(4242)
+    for seed, (n, kmax) in enumerate([(3, 2), (4, 3), (6, 5), (8, 7)]):
+        cx = synth.random_simplicial(3001 + seed, 4003 + seed, n, kmax, 900 + seed, float_weights=False)
+        f = g.uniform(-1, 1, (cx.k0, 1)).astype(np.float32)
+        for T in (2, 77, 512):
+            out = w.ecf_complex(torch.from_numpy(f).to(DEV), cells_of(cx), T,
+                                vweights=torch.from_numpy(cx.vweights).to(DEV)).cpu().numpy()
+            assert (out == oracle.ecf_complex(cx, f, T)).all(), (seed, T)
+    cx = synth.torus_mesh(301, 157, 3)
+    f = g.uniform(-1, 1, (cx.k0, 1)).astype(np.float32)
+    unit = synth.Complex(cx.coords, None, [synth.Cells(c.verts, None, c.dim) for c in cx.cells], cx.k0)
+    out = w.ecf_complex(torch.from_numpy(f).to(DEV), [(torch.from_numpy(c.verts).to(DEV), None, c.dim) for c in cx.cells],
+                        512).cpu().numpy()
+    assert (out == oracle.ecf_complex(unit, f, 512)).all()
+    big = synth.Complex(cx.coords, g.integers(-2**30, 2**30, cx.k0, dtype=np.int32),
+                        [synth.Cells(c.verts, g.integers(-2**30, 2**30, len(c.verts), dtype=np.int32), c.dim)
+                         for c in cx.cells], cx.k0)
+    out = w.ecf_complex(torch.from_numpy(f).to(DEV), cells_of(big), 300,
+                        vweights=torch.from_numpy(big.vweights).to(DEV)).cpu().numpy()
+    assert (out == oracle.ecf_complex(big, f, 300)).all()
+    mis = [(_misaligned(np.asarray(c.verts, np.int32)), torch.from_numpy(c.weights).to(DEV), c.dim) for c in cx.cells]
+    out = w.ecf_complex(torch.from_numpy(f).to(DEV), mis, 512, vweights=torch.from_numpy(cx.vweights).to(DEV))
+    assert (out.cpu().numpy() == oracle.ecf_complex(cx, f, 512)).all()
+    fi = g.integers(0, 256, (cx.k0, 1)).astype(np.float32)
+    out = w.ecf_complex(torch.from_numpy(fi).to(DEV), cells_of(cx), 256, vweights=torch.from_numpy(cx.vweights).to(DEV),
+                        lo=0.0, hi=255.0).cpu().numpy()
+    assert (out == oracle.ecf_complex(cx, fi, 256, lo=0.0, hi=255.0)).all()
