@@ -11,10 +11,10 @@
 // Passes: k_rcumsum (RC, one thread per row, q from T-1 down); per tile of 64 filters the
 // exact vertex-bin table VB (k_vbins of the forward for directions, k_vbins_f here for
 // given filter values); then k_grad_cells twice per tile (32 filters each, one per lane):
-// a warp takes 32 cells, the cell bin per lane is the max of its vertices' VB entries
+// a warp takes 16 cells, the cell bin per lane is the max of its vertices' VB entries
 // (eq. msi, exact because alpha is monotone), each lane gathers RC[bin] from a
-// shared-memory tile, and a 31-shuffle transpose-reduction leaves lane c with cell c's
-// sum over the 32 filters.  Tiles add into the fp64 gradient in a fixed order, so the
+// shared-memory tile, and a 31-shuffle transpose-reduction leaves lanes 2c, 2c+1 with
+// cell c's sum over the 32 filters.  Tiles add into the fp64 gradient in a fixed order, so the
 // result is deterministic.
 #include <cstdint>
 
@@ -22,7 +22,7 @@
 
 namespace wect {
 
-constexpr int kGradWarps = 8;
+constexpr int kGradWarps = 16;  // one 512-thread CTA per SM shares the RC tile
 
 
 __global__ void k_rcumsum(const double* __restrict__ G, int64_t rows, int T, double* __restrict__ RC) {
@@ -50,96 +50,87 @@ __global__ void __launch_bounds__(256) k_vbins_f(const float* __restrict__ f, in
   }
 }
 
-// lane c of the warp ends with sum over lanes of v[c] (31 shuffles, recursive halving)
-__device__ __forceinline__ double transpose_reduce(double (&v)[32], int lane) {
+// Recursive halving over 16 per-lane values v[c] (c = cell of the batch): after the
+// offsets 16, 8, 4, 2 lane l holds the partial sum of cell l >> 1 over half of the lanes,
+// and the last xor-1 step completes it in both lanes 2c and 2c + 1 (16 + 8 + 4 + 2 + 1
+// shuffles for 16 cells).
+__device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) {
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
+  for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
     const bool up = (lane & o) != 0;
 #pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const double send = up ? v[k] : v[k + o];
-      const double keep = up ? v[k + o] : v[k];
+    for (int k = 0; k < n; ++k) {
+      const double send = up ? v[k] : v[k + n];
+      const double keep = up ? v[k + n] : v[k];
       v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
   }
-  return v[0];
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// Bins of cells base + c, c < 32, for this lane's filter, 8 cells at a time with all
-// 8 * AR row loads in flight before the max (AR > 0: compile-time arity).
-template <int AR>
-__device__ __forceinline__ void cell_bins(const int (&ids)[8], int ar, const uint16_t* __restrict__ vb16,
-                                          int (&bins)[32], uint32_t& okmask) {
-  okmask = 0xffffffffu;
-#pragma unroll
-  for (int c0 = 0; c0 < 32; c0 += 8) {
-    int b[8][AR > 0 ? AR : 8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-#pragma unroll
-      for (int j = 0; j < (AR > 0 ? AR : 8); ++j) {
-        if (AR == 0 && j >= ar) { b[c][j] = 0; continue; }
-        const int id = __shfl_sync(0xffffffffu, ids[j], c0 + c);
-        if (id < 0) okmask &= ~(1u << (c0 + c));
-        b[c][j] = __ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      int m = b[c][0];
-#pragma unroll
-      for (int j = 1; j < (AR > 0 ? AR : 8); ++j) m = max(m, b[c][j]);
-      bins[c0 + c] = m;
-    }
-  }
-}
-
-// One pass: filters [row0, row0 + np) of the tile (np <= 32), lane = filter.
-// vb: the tile's VB table (u16 column (half * 32 + lane) of each 64-filter row).
+// One pass: filters [row0, row0 + np) of the tile (np <= 32), lane = filter; batches of
+// 16 cells, 8 cells x AR VB loads in flight at a time (AR = 0: runtime arity <= 8).
 template <bool SMEM_RC, int AR>
 __device__ __forceinline__ void grad_segment(const Seg& S, double* __restrict__ go, int64_t k0,
                                              const uint16_t* __restrict__ vb16, int np, const double* __restrict__ rcs,
                                              const double* __restrict__ RC, int row0, int T, int first, int64_t gw,
                                              int64_t nwarps, int lane) {
+  constexpr int MA = AR > 0 ? AR : 8;
   const int ar = AR > 0 ? AR : S.arity;
-  for (int64_t base = gw * 32; base < S.count; base += nwarps * 32) {
-    const int64_t mycell = base + lane;
-    int ids[8];
+  for (int64_t base = gw * 16; base < S.count; base += nwarps * 16) {
+    const int64_t mycell = base + (lane & 15);
+    int ids[MA];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < MA; ++j) {
       int id = 0;
       if (j < ar && mycell < S.count) {
         id = S.verts ? __ldg(S.verts + mycell * ar + j) : (int)mycell;
         if ((unsigned)id >= (unsigned)k0) {
-          atomicOr(&g_err_word, 1u);
+          if (lane < 16) atomicOr(&g_err_word, 1u);
           id = -1;
         }
       }
       ids[j] = id;
     }
-    int bins[32];
-    uint32_t okmask;
-    cell_bins<AR>(ids, ar, vb16, bins, okmask);
-    double v[32];
+    double v[16];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      double x = 0.0;
-      if (((okmask >> c) & 1u) && lane < np)
-        x = SMEM_RC ? rcs[bins[c] * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bins[c]);
-      v[c] = x;
+    for (int c0 = 0; c0 < 16; c0 += 8) {
+      int b[8][MA];
+      bool ok[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        ok[c] = true;
+#pragma unroll
+        for (int j = 0; j < MA; ++j) {
+          if (AR == 0 && j >= ar) { b[c][j] = 0; continue; }
+          const int id = __shfl_sync(0xffffffffu, ids[j], c0 + c);
+          ok[c] &= id >= 0;
+          b[c][j] = __ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        int bin = b[c][0];
+#pragma unroll
+        for (int j = 1; j < MA; ++j) bin = max(bin, b[c][j]);
+        double x = 0.0;
+        if (ok[c] && lane < np) x = SMEM_RC ? rcs[bin * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bin);
+        v[c0 + c] = x;
+      }
     }
-    const double sum = transpose_reduce(v, lane);
-    if (mycell < S.count) {
+    const double sum = transpose_reduce16(v, lane);
+    const int64_t cell = base + (lane >> 1);
+    if ((lane & 1) == 0 && cell < S.count) {
       const double gcell = S.sign < 0 ? -sum : sum;
-      go[mycell] = first ? gcell : go[mycell] + gcell;
+      go[cell] = first ? gcell : go[cell] + gcell;
     }
   }
 }
 
 template <bool SMEM_RC>
-__global__ void __launch_bounds__(kGradWarps * 32) k_grad_cells(Segs segs, int64_t k0, const uint32_t* __restrict__ vb,
-                                                                int half, int np, const double* __restrict__ RC,
-                                                                int row0, int T, GradOut gout, int first) {
+__global__ void __launch_bounds__(kGradWarps * 32, 1) k_grad_cells(Segs segs, int64_t k0, const uint32_t* __restrict__ vb,
+                                                                   int half, int np, const double* __restrict__ RC,
+                                                                   int row0, int T, GradOut gout, int first) {
   extern __shared__ __align__(16) double rcs[];  // [T][32]
   const int lane = threadIdx.x & 31;
   if (SMEM_RC) {
@@ -188,8 +179,8 @@ wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* 
   }
   int64_t maxc = 0;
   for (int i = 0; i < segs.nseg; ++i) maxc = segs.s[i].count > maxc ? segs.s[i].count : maxc;
-  int64_t want = (maxc + 32 * kGradWarps - 1) / (32 * kGradWarps);
-  const int per_sm = use_smem ? (int)((200 * 1024) / smem > 4 ? 4 : ((200 * 1024) / smem < 1 ? 1 : (200 * 1024) / smem)) : 4;
+  int64_t want = (maxc + 16 * kGradWarps - 1) / (16 * kGradWarps);
+  const int per_sm = use_smem ? (int)((200 * 1024) / smem > 2 ? 2 : ((200 * 1024) / smem < 1 ? 1 : (200 * 1024) / smem)) : 2;
   const int ctas = (int)(want < (int64_t)num_sms * per_sm ? (want < 1 ? 1 : want) : (int64_t)num_sms * per_sm);
   wect_status s = WECT_OK;
   for (int t0 = 0; t0 < Dc && s == WECT_OK; t0 += 64) {
