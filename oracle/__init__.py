@@ -49,6 +49,7 @@ def lib():
         L.orc_wect_images.argtypes = [vp, i64, i32, vp, vp, i32, i32, d, ctypes.c_int, vp]
         L.orc_wect_images.restype = ctypes.c_int
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_set_num_threads.argtypes = [ctypes.c_int]
         _LIB = L
     return _LIB
 
@@ -59,6 +60,10 @@ def _p(a: Optional[np.ndarray]):
 
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(int(n))
 
 
 # ----------------------------------------------------------------- primitives

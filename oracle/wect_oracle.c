@@ -353,6 +353,15 @@ ORC_API int orc_wect_images(const uint8_t* img, int64_t B, int32_t ndim, const i
   return rc;
 }
 
+/* thread count of the OpenMP loops (bench: the single-core baseline) */
+ORC_API void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 ORC_API int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
