@@ -110,3 +110,55 @@ def wect_complex_sharded(coords, cells: Sequence[Tuple], dirs, T: int, *, gather
         ref = compute(coords, cells, dirs, T, 0, 1, **kw)
         local = ref[:0]
     return gather_rows(local, D, 0, group) if gather else local
+
+
+def _lib_ecf_images(img, T, **kw):
+    from . import ecf_images
+
+    return ecf_images(img, T, **kw)
+
+
+def ecf_images_sharded(img: torch.Tensor, T: int, *, gather: bool = True, group=None,
+                       compute: Optional[Callable] = None, **kw) -> torch.Tensor:
+    """Image ECF (ecf_images, NEXT-1) of a batch across ranks: every image is its own complex
+    (its own M, or the caller's fixed grid), so rank r computes images shard_range(B, world, r)
+    with no exchange; gather=True assembles [B, T] on every rank (all_gather)."""
+    compute = compute or _lib_ecf_images
+    world, rank = _world(group)
+    B = int(img.shape[0])
+    lo, hi = shard_range(B, world, rank)
+    local = compute(img[lo:hi].contiguous(), T, **kw)
+    return gather_rows(local, B, 0, group) if gather else local
+
+
+def _lib_backward(coords, cells, dirs, T, G_rows, d_begin, d_count, **kw):
+    from . import wect_complex_backward
+
+    return wect_complex_backward(coords, cells, dirs, T, G_rows, d_begin=d_begin, d_count=d_count, **kw)
+
+
+def wect_complex_backward_sharded(coords, cells: Sequence[Tuple], dirs, T: int, G, *, group=None,
+                                  compute: Optional[Callable] = None, **kw):
+    """Weights gradient (NEXT-3) of one complex, direction-sharded.  dL/dw(s) is a SUM over
+    the direction rows p (include/wect.h), so rank r computes the partial gradient of its rows
+    shard_range(D, world, r) (M over ALL directions, reading A2) and the partials are
+    all-reduced (SUM) -- the one real exchange step of the path.  G: the full [D, T] fp64.
+    Returns (grad_vweights, [grad_cells_i]) on every rank.  Exact for integer-valued G; for
+    general G the cross-rank sum adds one more reassociation to reading A13."""
+    compute = compute or _lib_backward
+    world, rank = _world(group)
+    D = int(dirs.shape[0])
+    lo, hi = shard_range(D, world, rank)
+    if hi > lo:
+        gv, gc = compute(coords, cells, dirs, T, G[lo:hi].contiguous(), lo, hi - lo, **kw)
+    else:  # more ranks than directions: a zero partial
+        gv, gc = compute(coords, cells, dirs, T, G[:1].contiguous(), 0, 1, **kw)
+        gv = torch.zeros_like(gv)
+        gc = [torch.zeros_like(g) for g in gc]
+    if world > 1:
+        flat = torch.cat([gv.reshape(-1)] + [g.reshape(-1) for g in gc])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        sizes = [gv.numel()] + [g.numel() for g in gc]
+        parts = list(torch.split(flat, sizes))
+        gv, gc = parts[0].view_as(gv), [p.view_as(g) for p, g in zip(parts[1:], gc)]
+    return gv, gc

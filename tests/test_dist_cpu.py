@@ -13,7 +13,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2511_03909_b200.dist import gather_rows, shard_range, wect_complex_sharded, wect_images_sharded
+from paper_2511_03909_b200.dist import (ecf_images_sharded, gather_rows, shard_range, wect_complex_backward_sharded,
+                                        wect_complex_sharded, wect_images_sharded)
 
 
 def test_shard_range_partitions():
@@ -39,6 +40,19 @@ def _oracle_complex(coords, cells, dirs, T, d_begin, d_count, **kw):
     cx = synth.Complex(coords, kw["vweights"], [synth.Cells(v, w, d) for v, w, d in cells], coords.shape[0])
     full = oracle.wect_complex(cx, dirs, T)
     return torch.from_numpy(full[d_begin:d_begin + d_count].copy())
+
+
+def _oracle_ecf_images(img, T, **kw):
+    return torch.from_numpy(oracle.ecf_images(img.numpy(), T, kw.get("lo", 0.0), kw.get("hi", 0.0)))
+
+
+def _oracle_backward(coords, cells, dirs, T, G_rows, d_begin, d_count, **kw):
+    """the oracle's closed-form gradient of the rows [d_begin, d_begin + d_count), M over ALL rows"""
+    cx = synth.Complex(coords, None, [synth.Cells(v, None, d) for v, _, d in cells], coords.shape[0])
+    fv = oracle.heights(coords, dirs)
+    M = oracle.maxheight(fv)
+    gv, gc = oracle.wecfs_grad(fv[:, d_begin:d_begin + d_count], cx, T, -M, M, np.asarray(G_rows))
+    return torch.from_numpy(gv), [torch.from_numpy(g) for g in gc]
 
 
 def _free_port():
@@ -68,8 +82,17 @@ def _worker(rank, world, port, q):
         d3[4] *= 3.0  # the row that sets M lives on the last rank
         cref = oracle.wect_complex(cx, d3, 12)
         c = wect_complex_sharded(cx.coords, cells, d3, 12, compute=_oracle_complex, vweights=cx.vweights)
+        # image ECF (NEXT-1): batch shards, no exchange
+        eimg = torch.from_numpy(g.integers(0, 256, (5, 6, 8), dtype=np.uint8))
+        eref = oracle.ecf_images(eimg.numpy(), 32, 0.0, 255.0)
+        e = ecf_images_sharded(eimg, 32, compute=_oracle_ecf_images, lo=0.0, hi=255.0)
+        # weights gradient (NEXT-3): direction shards, partial gradients all-reduced (SUM)
+        G = torch.from_numpy(g.integers(-3, 4, size=(5, 12)).astype(np.float64))
+        gv_ref, gc_ref = oracle.wect_complex_grad(cx, d3, 12, G.numpy())
+        gv, gc = wect_complex_backward_sharded(cx.coords, cells, d3, 12, G, compute=_oracle_backward)
+        gok = np.array_equal(gv.numpy(), gv_ref) and all(np.array_equal(a_.numpy(), b_) for a_, b_ in zip(gc, gc_ref))
         q.put((rank, bool(torch.equal(a, ref)), bool(torch.equal(b, ref)), bool(torch.equal(loc, ref[lo:hi])),
-               bool(np.array_equal(c.numpy(), cref))))
+               bool(np.array_equal(c.numpy(), cref)), bool(np.array_equal(e.numpy(), eref)), bool(gok)))
     finally:
         dist.destroy_process_group()
 

@@ -105,3 +105,20 @@ def test_backward_mesh_euler_identity_at_scale():
     for x, g in zip(cx.cells, gc):
         lin += float((x.weights.astype(np.float64) * g.cpu().numpy()).sum())
     assert lin == L
+
+
+def test_sharded_entry_points_single_rank_use_the_library():
+    """dist.wect_complex_backward_sharded / ecf_images_sharded without a process group:
+    the default compute is the CUDA library (no oracle, no fallback)."""
+    from paper_2511_03909_b200.dist import ecf_images_sharded, wect_complex_backward_sharded
+
+    cx = synth.torus_mesh(7, 9, 2)
+    dirs = torch.from_numpy(synth.directions_sphere(20, 3, 6400)).to(DEV)
+    G = torch.from_numpy(np.random.default_rng(4).integers(-3, 4, size=(20, 50)).astype(np.float64)).to(DEV)
+    coords = torch.from_numpy(cx.coords).to(DEV)
+    gv, gc = wect_complex_backward_sharded(coords, _cells(cx), dirs, 50, G)
+    ov, oc = oracle.wect_complex_grad(cx, dirs.cpu().numpy(), 50, G.cpu().numpy())
+    _check(gv, gc, ov, oc, G.cpu().numpy(), True)
+    img = torch.from_numpy(synth.images_u8(9, (28, 28), 6500)).to(DEV)
+    e = ecf_images_sharded(img, 256, lo=0.0, hi=255.0)
+    assert (e.cpu().numpy() == oracle.ecf_images(img.cpu().numpy(), 256, 0.0, 255.0)).all()
