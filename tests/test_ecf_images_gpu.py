@@ -98,3 +98,21 @@ def test_ecf_images_large_path_sampled():
     out = gpu(img, 256, lo=0.0, hi=255.0)
     ref = oracle.ecf_images(img, 256, 0.0, 255.0)
     assert (out == ref).all()
+
+
+def test_ecf_images_errors_and_row_args():
+    zero = torch.zeros((2, 4, 4), dtype=torch.uint8, device=DEV)
+    from paper_2511_03909_b200 import _lib as L
+    import ctypes
+
+    g = L.wect_grid(8, 1, 0, 0.0, 0.0, 0.0, 0)  # d_begin != 0: one filter per image
+    out = torch.empty((2, 8), dtype=torch.int32, device=DEV)
+    dims = (ctypes.c_int64 * 2)(4, 4)
+    st = L.load().ecf_images(zero.data_ptr(), 2, 2, dims, ctypes.byref(g), out.data_ptr(), L.I32, None)
+    assert st == L.EINVAL
+    g = L.wect_grid(70000, 0, 0, 0.0, 0.0, 0.0, 0)  # T > 65536
+    st = L.load().ecf_images(zero.data_ptr(), 2, 2, dims, ctypes.byref(g), out.data_ptr(), L.I32, None)
+    assert st == L.ENOTSUP
+    g = L.wect_grid(8, 0, 0, 0.0, 0.0, 0.0, 0)
+    st = L.load().ecf_images(zero.data_ptr(), 2, 4, dims, ctypes.byref(g), out.data_ptr(), L.I32, None)  # ndim 4
+    assert st == L.EINVAL

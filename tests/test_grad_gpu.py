@@ -122,3 +122,36 @@ def test_sharded_entry_points_single_rank_use_the_library():
     img = torch.from_numpy(synth.images_u8(9, (28, 28), 6500)).to(DEV)
     e = ecf_images_sharded(img, 256, lo=0.0, hi=255.0)
     assert (e.cpu().numpy() == oracle.ecf_images(img.cpu().numpy(), 256, 0.0, 255.0)).all()
+
+
+def test_backward_edge_cases_and_errors():
+    from paper_2511_03909_b200 import _lib
+
+    cx = synth.torus_mesh(5, 6, 1)
+    dirs = synth.directions_sphere(7, 3, 6600)
+    cells = [(c.verts, None, c.dim) for c in cx.cells]
+    G = np.ones((7, 9))
+    # T < 2, bad row range, NULL G
+    with pytest.raises(_lib.WectError):
+        w.wect_complex_backward(cx.coords, cells, dirs, 1, np.ones((7, 1)))
+    with pytest.raises(_lib.WectError):
+        w.wect_complex_backward(cx.coords, cells, dirs, 9, G, d_begin=5, d_count=5)
+    # arity 9 cells: not supported by the backward (documented)
+    wide = [(np.zeros((3, 9), np.int32), None, 8)]
+    with pytest.raises(_lib.WectError):
+        w.wect_complex_backward(cx.coords, wide, dirs, 9, G)
+    # out-of-range vertex index: reported by sync_status, the cell gets no gradient
+    bad = [(np.array([[0, 1], [2, cx.k0 + 5]], np.int32), None, 1)]
+    w.wect_complex_backward(cx.coords, bad, dirs, 9, G)
+    with pytest.raises(_lib.WectError):
+        w.sync_status()
+    # G = 0 -> zero gradient; single direction; T = 2
+    gv, gc = w.wect_complex_backward(cx.coords, cells, dirs[:1], 2, np.zeros((1, 2)))
+    assert float(np.abs(gv.numpy()).max()) == 0.0 and all(float(np.abs(g.numpy()).max()) == 0.0 for g in gc)
+    # top-bin-only G: every gradient is its sign times the number of rows (all cells land in bins <= T-1)
+    Gt = np.zeros((7, 9))
+    Gt[:, -1] = 1.0
+    gv, gc = w.wect_complex_backward(cx.coords, cells, dirs, 9, Gt)
+    assert (gv.numpy() == 7.0).all()
+    for (v, _, d), g in zip(cells, gc):
+        assert (g.numpy() == (7.0 if d % 2 == 0 else -7.0)).all()
