@@ -270,3 +270,42 @@ def ecf_complex_grad(cx, fvals32: np.ndarray, T: int, G: np.ndarray, lo: float =
         M = maxheight(fv)
         lo, hi = -M, M
     return wecfs_grad(fv, cx, T, lo, hi, G)
+
+
+# ------------------------------------------------ Freudenthal images (NEXT-2)
+def freudenthal_complex(img: np.ndarray):
+    """Explicit weighted Freudenthal complex of ONE 2-D image: pixels
+    are vertices at the grid coordinates of reading A3; edges are the horizontal, vertical
+    and (r,c)-(r+1,c+1) diagonal pairs; each unit square splits along that diagonal into
+    {(r,c),(r,c+1),(r+1,c+1)} and {(r,c),(r+1,c),(r+1,c+1)}; vertex weight = intensity,
+    every other simplex's weight = max of its vertices' weights."""
+    import synth  # generator container type only
+
+    im = np.ascontiguousarray(img, np.uint8)
+    H, W = im.shape
+    idx = np.arange(H * W, dtype=np.int64).reshape(H, W)
+    flat = im.reshape(-1).astype(np.int64)
+    e = [np.stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()], 1),      # horizontal
+         np.stack([idx[:-1, :].ravel(), idx[1:, :].ravel()], 1),      # vertical
+         np.stack([idx[:-1, :-1].ravel(), idx[1:, 1:].ravel()], 1)]   # diagonal (r,c)-(r+1,c+1)
+    edges = np.concatenate(e, 0)
+    t_up = np.stack([idx[:-1, :-1].ravel(), idx[:-1, 1:].ravel(), idx[1:, 1:].ravel()], 1)
+    t_lo = np.stack([idx[:-1, :-1].ravel(), idx[1:, :-1].ravel(), idx[1:, 1:].ravel()], 1)
+    tris = np.concatenate([t_up, t_lo], 0)
+    ew = flat[edges].max(axis=1) if len(edges) else np.zeros(0, np.int64)
+    tw = flat[tris].max(axis=1) if len(tris) else np.zeros(0, np.int64)
+    cells = [synth.Cells(edges.astype(np.int32).reshape(-1, 2), ew.astype(np.int32), 1),
+             synth.Cells(tris.astype(np.int32).reshape(-1, 3), tw.astype(np.int32), 2)]
+    return synth.Complex(grid_coords((H, W)), flat.astype(np.int32), cells, H * W, is_float=False)
+
+
+def wect_images_freudenthal(img: np.ndarray, dirs: np.ndarray, T: int, maxheight_override: float = 0.0,
+                            naive: bool = False) -> np.ndarray:
+    """O2 (or O1) WECT of a batch [B, H, W] of u8 images as Freudenthal complexes, M over
+    ALL directions of the (image-independent) grid (reading A2): int64 [B, D, T]."""
+    img = np.ascontiguousarray(img, np.uint8)
+    out = np.zeros((img.shape[0], dirs.shape[0], T), np.int64)
+    for b in range(img.shape[0]):
+        cx = freudenthal_complex(img[b])
+        out[b] = wect_complex(cx, dirs, T, maxheight_override, naive)
+    return out
