@@ -74,6 +74,10 @@ typedef enum { WECT_U8 = 1, WECT_I32 = 2, WECT_I64 = 3, WECT_F32 = 4, WECT_F64 =
                               differ from reading A1 for heights within rounding of a bin edge) */
 #define WECT_TIME_MAIN 4u  /* instrumentation: record CUDA events around the call's dominant kernel on
                               `stream` (read with wect_stats); adds no synchronisation */
+#define WECT_FREUDENTHAL 8u /* wect_images, ndim = 2 only: the image as a weighted Freudenthal complex
+                               instead of a cubical one -- horizontal, vertical
+                              and (r,c)-(r+1,c+1) diagonal edges, two triangles per unit square, each
+                              simplex weighted by the max of its vertices, sign (-1)^dim */
 
 /* One dimension i >= 1 of K: the pair (i-SimplexVertices, i-SimplexWeights) of the
  * Complex list.  verts: [count, arity] int32 row-major, values in [0, k0).
@@ -137,7 +141,9 @@ WECT_API wect_status wect_complex(const wect_complex_desc* K, const float* dirs,
  * column -> axis 0, row -> axis 1, slice -> axis 2.  No cell lists touch memory.
  * img: [B, dims...] uint8.  dims: HOST array.  dirs: [D, ndim] fp32.
  * out: [B, d_count, T] of WECT_I32 (refused with WECT_EOVERFLOW when
- * 255 * #cells >= 2^31) or WECT_I64. */
+ * 255 * #cells >= 2^31) or WECT_I64.
+ * grid->flags & WECT_FREUDENTHAL (ndim = 2): the Freudenthal triangulation of each image
+ * instead (same vertices and coordinates, same M; every simplex binned exactly). */
 WECT_API wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims, const float* dirs,
                         int32_t D, const wect_grid* grid, void* out, wect_dtype odtype, void* stream);
 

@@ -21,7 +21,7 @@ from typing import Iterable, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import FP32_ONLY, TIME_MAIN, VALIDATE, WectError  # noqa: F401
+from ._lib import FP32_ONLY, FREUDENTHAL, TIME_MAIN, VALIDATE, WectError  # noqa: F401
 
 __all__ = ["wect_images", "ecf_images", "wect_complex", "ecf_complex", "wect_complex_backward", "ecf_complex_backward", "wect_maxheight", "sync_status", "repair_count",
            "stats", "WectError", "VALIDATE", "FP32_ONLY", "TIME_MAIN", "load"]
@@ -97,10 +97,14 @@ def _alloc_out(shape, torch_dtype_name, dev, out):
 
 
 def wect_images(img, dirs, T: int, *, d_begin: int = 0, d_count: int = 0, maxheight: float = 0.0, lo: float = 0.0,
-                hi: float = 0.0, out_dtype: str = "int32", out=None, flags: int = 0, stream=None):
-    """WECT of a batch of uint8 images [B, H, W] or volumes [B, Z, Y, X].
+                hi: float = 0.0, out_dtype: str = "int32", out=None, flags: int = 0, freudenthal: bool = False,
+                stream=None):
+    """WECT of a batch of uint8 images [B, H, W] or volumes [B, Z, Y, X], as
+    cubical complexes, or (freudenthal=True, 2-D) as Freudenthal triangulations.
 
     Returns [B, d_count or D - d_begin, T] (int32 or int64)."""
+    if freudenthal:
+        flags |= _lib.FREUDENTHAL
     L = _lib.load()
     img = _as(img, np.uint8, "uint8")
     dirs = _as(dirs, np.float32, "float32")

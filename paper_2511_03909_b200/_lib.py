@@ -16,7 +16,7 @@ STATUS_NAMES = {0: "WECT_OK", -1: "WECT_EINVAL", -2: "WECT_ERANGE", -3: "WECT_EO
 # wect_dtype
 U8, I32, I64, F32, F64 = 1, 2, 3, 4, 5
 # flags
-VALIDATE, FP32_ONLY, TIME_MAIN = 1, 2, 4
+VALIDATE, FP32_ONLY, TIME_MAIN, FREUDENTHAL = 1, 2, 4, 8
 
 EXPORTS = ("wect_complex", "wect_images", "ecf_complex", "ecf_images", "wect_complex_backward", "ecf_complex_backward", "wect_maxheight", "wect_sync_status", "wect_last_error",
            "wect_repair_count", "wect_stats", "wect_abi_version")

@@ -84,6 +84,10 @@ wect_status launch_ecf_images(const uint8_t* img, int64_t B, int ndim, const int
 wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* coords, int64_t k0, const float* fsrc,
                                 int m_or_D, int d_begin, int Dc, int T, const GridParams* gp, const double* G,
                                 const GradOut& gout, cudaStream_t st, int num_sms);
+size_t freud_scratch_per_image(int H, int W);
+wect_status launch_freud(const uint8_t* img, int64_t b0, int64_t nb, int H, int W, const float* dirs, int d_begin,
+                         int Dc, int T, const GridParams* gp, int16_t* w6, unsigned long long* diff, cudaStream_t st,
+                         int num_sms);
 wect_status launch_finalize(const void* diff, bool is_float, int64_t rows, int T, void* out, wect_dtype odtype,
                             cudaStream_t st);
 
@@ -276,6 +280,13 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
     nv *= dims[i];
     ncells *= 2 * dims[i] - 1;
   }
+  const bool freud = (grid->flags & WECT_FREUDENTHAL) != 0;
+  if (freud) {
+    if (ndim != 2) return fail(WECT_ENOTSUP, "WECT_FREUDENTHAL needs 2-D images");
+    // V + E + F of the Freudenthal complex: HW + [H(W-1) + W(H-1) + (H-1)(W-1)] + 2(H-1)(W-1)
+    const int64_t H = dims[0], W = dims[1];
+    ncells = H * W + H * (W - 1) + W * (H - 1) + 3 * (H - 1) * (W - 1);
+  }
   int d_begin, Dc;
   wect_status rs = resolve_rows(grid, D, &d_begin, &Dc);
   if (rs != WECT_OK) return rs;
@@ -283,8 +294,8 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   if (odtype == WECT_I32 && 255.0 * (double)ncells >= 2147483648.0)
     return fail(WECT_EOVERFLOW, "int32 output cannot bound 255 * %lld cells", (long long)ncells);
   if (B > 0 && Dc > 0 && (!img || !out)) return fail(WECT_EINVAL, "img/out is NULL");
-  const bool sweep = sweep2d_supported(ndim, dims, grid->T);
-  if (!sweep && grid->T > 1024) return fail(WECT_ENOTSUP, "T > 1024 needs the sweep path (2D, H*W <= 1024)");
+  const bool sweep = !freud && sweep2d_supported(ndim, dims, grid->T);
+  if (!sweep && grid->T > 1024) return fail(WECT_ENOTSUP, "T > 1024 needs the sweep path (2D cubical, H*W <= 1024)");
   if (B == 0 || Dc == 0) return WECT_OK;
 
   const int nsm = num_sms_current();
@@ -297,7 +308,22 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging", __FILE__, __LINE__);
   wect_status s = launch_grid_params(ndim, dims, ddirs, D, *grid, gp, st);
   if (s != WECT_OK) return s;
-  if (sweep) {
+  if (freud) {
+    const size_t nbins = (size_t)B * Dc * grid->T;
+    unsigned long long* diff = (unsigned long long*)ar.alloc(nbins * 8);
+    const int64_t per_img = (int64_t)freud_scratch_per_image((int)dims[0], (int)dims[1]);
+    int64_t chunk = ((int64_t)1 << 30) / per_img;
+    chunk = chunk < 1 ? 1 : (chunk > 65535 ? 65535 : chunk);
+    if (chunk > B) chunk = B;
+    int16_t* w6 = (int16_t*)ar.alloc((size_t)chunk * per_img);
+    if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
+    WECT_CUDA_TRY(cudaMemsetAsync(diff, 0, nbins * 8, st));
+    for (int64_t b0 = 0; b0 < B && s == WECT_OK; b0 += chunk) {
+      const int64_t nb = B - b0 < chunk ? B - b0 : chunk;
+      s = launch_freud(dimg, b0, nb, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, w6, diff, st, nsm);
+    }
+    if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
+  } else if (sweep) {
     void* scr = ar.alloc(sweep2d_scratch_bytes((int)nv, Dc, grid->T));
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
     s = launch_sweep2d(dimg, B, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, scr, ov.dev, odtype, st,
