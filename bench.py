@@ -9,7 +9,7 @@ wect_images call over the batch = every row of SURVEY.md section 8(a): grid M
 kernel (a0, a4-a7: implicit cells, max rule, signed regrouped accumulation,
 cumsum, 1.97 GB output write).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx|ecfimg|ecfimg1k|bwd3|bwd4] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx|ecfimg|ecfimg1k|bwd3|bwd4|freud] [--impl reference]
 
 Multi-GPU (torchrun, one rank per GPU): images are sharded by batch with no data-path
 collective (weak scaling: every rank runs its own 60,000-image shard); times are the
@@ -120,6 +120,16 @@ class ClockSampler:
 # --------------------------------------------------------------- workloads
 def workload(cfg: str, rank: int):
     """Returns a dict describing the per-rank workload (host arrays)."""
+    if cfg == "freud":
+        # the cfg2 batch as Freudenthal triangulations (SURVEY §8(f) NEXT-2, P:210-215)
+        wl = workload("1", rank)
+        H, W = wl["img"].shape[1:]
+        ncells = H * W + H * (W - 1) + W * (H - 1) + 3 * (H - 1) * (W - 1)
+        D = wl["dirs"].shape[0]
+        wl.update(kind="images", name="freudenthal_mnist60k", freudenthal=True, updates=wl["B"] * ncells * D,
+                  atomics=wl["B"] * H * W * 6 * D,
+                  desc=wl["desc"].replace("u8 images", "u8 images as Freudenthal complexes"))
+        return wl
     if cfg in ("1", "0", "2"):
         c = int(cfg)
         spec = dict(synth.CONFIGS[c])
@@ -215,7 +225,8 @@ def run_ours(args, rank, world, local_rank):
                             dtype=getattr(torch, wl["out_dtype"]), device=dev)
 
         def step(flags=0):
-            w.wect_images(img_d, dirs_d, wl["T"], out_dtype=wl["out_dtype"], out=out_d, flags=flags)
+            w.wect_images(img_d, dirs_d, wl["T"], out_dtype=wl["out_dtype"], out=out_d, flags=flags,
+                          freudenthal=wl.get("freudenthal", False))
     else:
         cx = wl["cx"]
         cells = [(torch.from_numpy(c.verts).to(dev), None if c.weights is None else torch.from_numpy(c.weights).to(dev),
@@ -299,6 +310,8 @@ def run_ours(args, rank, world, local_rank):
     D = wl["dirs"].shape[0] if "dirs" in wl else 1
     if wl["kind"] == "ecfimg":
         kname, bound = ("k_ecf_img2d_w4", "hbm") if args.config == "ecfimg" else ("k_ecf_img_hist", "alu")
+    elif wl.get("freudenthal"):
+        kname, bound = "k_freud_hist", "alu"
     elif wl["kind"] == "images" and args.config in ("0", "1"):
         kname, bound = "k_sweep2d", "hbm"
     elif wl["kind"] == "images":
@@ -379,14 +392,15 @@ def run_ours(args, rank, world, local_rank):
         img_h = torch.from_numpy(wl["img"]).pin_memory()
         dirs_h = torch.from_numpy(wl["dirs"])
         out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
+        fr = wl.get("freudenthal", False)
         for _ in range(2):
-            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h)
+            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h, freudenthal=fr)
         ke = max(1, min(5, K))
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         for _ in range(ke):
-            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h)
+            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h, freudenthal=fr)
         e2e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -461,6 +475,15 @@ def cpu_baseline(wl, budget_s=15.0, max_units=None):
         t = time.perf_counter() - t0
         return {"value": 1.0 / (t * D / nd), "unit": wl["unit"], "cores": cores, "kind": "oracle",
                 "sample": f"O2 on {nd} of {D} directions of the volume ({t:.1f} s), scaled by D/{nd}"}
+    if wl.get("freudenthal"):
+        done, t = 0, 0.0
+        while done < wl["B"] and t < budget_s:
+            t0 = time.perf_counter()
+            oracle.wect_images_freudenthal(wl["img"][done:done + 50], wl["dirs"], wl["T"])
+            t += time.perf_counter() - t0
+            done += 50
+        return {"value": done / t, "unit": wl["unit"], "cores": cores, "kind": "oracle",
+                "sample": f"O2 on the explicit Freudenthal complexes of images [0, {done}) ({t:.1f} s)"}
     if wl["kind"] == "images" and wl["img"].shape[1:] == (28, 28):
         # all host cores, then one core (the paper's single-core comparison)
         res = cpu_baseline(dict(wl, kind="images_batch"), budget_s, max_units)
@@ -569,7 +592,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4), ecfx, ecfimg, ecfimg1k, bwd3 or bwd4")
+    ap.add_argument("--config", default="1", help="BASELINE configs index (0-4), ecfx, ecfimg, ecfimg1k, bwd3, bwd4 or freud")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
