@@ -62,8 +62,8 @@ wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs,
 bool sweep2d_supported(int ndim, const int64_t* dims, int T);
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
                            const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
-                           int num_sms);
-size_t sweep2d_scratch_bytes(int HW, int Dc, int T);
+                           int num_sms, int freud);
+size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud);
 wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndim, const int64_t* dims,
                              const float* dirs, int d_begin, int Dc, int T, const GridParams* gp, int16_t* cwo,
                              unsigned long long* diff, cudaStream_t st, int num_sms);
@@ -294,7 +294,7 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   if (odtype == WECT_I32 && 255.0 * (double)ncells >= 2147483648.0)
     return fail(WECT_EOVERFLOW, "int32 output cannot bound 255 * %lld cells", (long long)ncells);
   if (B > 0 && Dc > 0 && (!img || !out)) return fail(WECT_EINVAL, "img/out is NULL");
-  const bool sweep = !freud && sweep2d_supported(ndim, dims, grid->T);
+  const bool sweep = sweep2d_supported(ndim, dims, grid->T) && !(freud && getenv("WECT_FREUD_HIST"));
   if (!sweep && grid->T > 1024) return fail(WECT_ENOTSUP, "T > 1024 needs the sweep path (2D cubical, H*W <= 1024)");
   if (B == 0 || Dc == 0) return WECT_OK;
 
@@ -308,7 +308,7 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging", __FILE__, __LINE__);
   wect_status s = launch_grid_params(ndim, dims, ddirs, D, *grid, gp, st);
   if (s != WECT_OK) return s;
-  if (freud) {
+  if (freud && !sweep) {
     const size_t nbins = (size_t)B * Dc * grid->T;
     unsigned long long* diff = (unsigned long long*)ar.alloc(nbins * 8);
     const int64_t per_img = (int64_t)freud_scratch_per_image((int)dims[0], (int)dims[1]);
@@ -324,10 +324,10 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
     }
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
   } else if (sweep) {
-    void* scr = ar.alloc(sweep2d_scratch_bytes((int)nv, Dc, grid->T));
+    void* scr = ar.alloc(sweep2d_scratch_bytes((int)nv, Dc, grid->T, freud ? 1 : 0));
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
     s = launch_sweep2d(dimg, B, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, scr, ov.dev, odtype, st,
-                       nsm);
+                       nsm, freud ? 1 : 0);
   } else {
     const size_t nbins = (size_t)B * Dc * grid->T;
     unsigned long long* diff = (unsigned long long*)ar.alloc(nbins * 8);

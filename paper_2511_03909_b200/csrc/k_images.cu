@@ -118,10 +118,29 @@ __host__ __device__ constexpr int sweep_prog_words(int HW, int T) {
   return 4 * sweep_prog_packets(HW, T) + sweep_prog_packets(HW, T) / 4;
 }
 
+// Freudenthal designated vertex (offset index: 0 self, 1 X = (r,c+1), 2 Y = (r+1,c),
+// 3 D = (r+1,c+1)) of simplex type t (1 e_x, 2 e_y, 3 e_diag, 4 U, 5 L) in chamber (A, B, C)
+// = (s_x > 0, s_y > 0, s_x + s_y > 0); its vertex set as a bit mask over {self, X, Y, D}.
+__host__ __device__ __forceinline__ int freud_des(int t, int A, int B, int C) {
+  switch (t) {
+    case 1: return A ? 1 : 0;
+    case 2: return B ? 2 : 0;
+    case 3: return C ? 3 : 0;
+    case 4: return (B && C) ? 3 : ((A && !B) ? 1 : 0);
+    case 5: return (A && C) ? 3 : ((B && !A) ? 2 : 0);
+  }
+  return 0;
+}
+__host__ __device__ __forceinline__ int freud_mask(int t) {
+  constexpr int m[6] = {0x1, 0x3, 0x5, 0x9, 0xB, 0xD};
+  return m[t];
+}
+
 __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __restrict__ dirs, int d_begin, int Dc,
                                                 const GridParams* __restrict__ gp, uint32_t* __restrict__ prog,
                                                 int* __restrict__ prog_len, int* __restrict__ qlist,
-                                                int* __restrict__ qcount) {
+                                                int* __restrict__ qcount, int freud, int4* __restrict__ corr,
+                                                int* __restrict__ ncorr, int corr_cap) {
   // smem: counts[T], base[T], meta[Lp] (emit | flag << 16), vbin[HW] (u16)
   extern __shared__ int sh[];
   const GridParams g = *gp;
@@ -174,11 +193,34 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
     pk = (pk + 3) & ~3;  // whole groups of 4 packets (the tail packets are padding, no flags)
     npk_total = pk;
     prog_len[dl] = pk;
-    int o = (sx > 0.f ? 1 : 0) | (sy > 0.f ? 2 : 0);
+    // cubical: quadrant (s_x > 0) | (s_y > 0) << 1; Freudenthal: chamber | (s_x + s_y > 0) << 2
+    int o = (sx > 0.f ? 1 : 0) | (sy > 0.f ? 2 : 0) | ((freud && sx + sy > 0.f) ? 4 : 0);
     int slot = atomicAdd(&qcount[o], 1);
     qlist[o * Dc + slot] = dl;
   }
   __syncthreads();
+  if (freud) {
+    // Simplices whose chamber-designated vertex does not carry the simplex's max exact bin
+    // (only possible through the rounded diagonal comparison): the sweep counts them from
+    // bin lo = vbin[designated]; record [lo, hi) so k_sweep_fix moves them to hi.
+    const int A = sx > 0.f, B = sy > 0.f, C = (sx + sy) > 0.f;
+    for (int i = threadIdx.x; i < 5 * HW; i += blockDim.x) {
+      const int u = i / 5, t = 1 + (i - u * 5), r = u / W, c = u - r * W;
+      const bool rt = c + 1 < W, dn = r + 1 < H;
+      if ((t == 1 && !rt) || (t == 2 && !dn) || (t >= 3 && !(rt && dn))) continue;
+      const int off[4] = {0, 1, W, W + 1};
+      const int mask = freud_mask(t);
+      int hi = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (mask >> k & 1) hi = max(hi, (int)vbin[u + off[k]]);
+      const int lo = vbin[u + off[freud_des(t, A, B, C)]];
+      if (hi > lo) {
+        const int slot = atomicAdd(ncorr, 1);
+        if (slot < corr_cap) corr[slot] = make_int4(dl, u, t, lo | (hi << 16));
+      }
+    }
+  }
   for (int v = threadIdx.x; v < HW; v += blockDim.x) {  // ids: any order within a bin
     const int bq = vbin[v];
     const int r = atomicAdd(&counts[bq], -1) - 1;
@@ -335,7 +377,30 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
   }
 }
 
-template <typename OutT>
+// Freudenthal combined weight of vertex (r, c) for chamber (A, B, C): the signed weights of
+// the simplices (anchored at v - delta) whose designated vertex is v (freud_des), packed
+// u16x2 for images (2l, 2l+1): positives (vertex, U, L) minus negatives (3 edges), each
+// sum <= 765 per half.  p0 = this lane's pixel pair of vertex v in the staged rows.
+__device__ __forceinline__ uint32_t freud_cw(const uint8_t* p0, int r, int c, int H, int W, int A, int B, int C) {
+  auto P = [&](int dr, int dc) -> uint32_t {
+    return __byte_perm(*(const uint16_t*)(p0 + (dr * W + dc) * kPixStride), 0, 0x4140);
+  };
+  const bool up = r > 0, dn = r + 1 < H, lf = c > 0, rt = c + 1 < W;
+  const uint32_t a = P(0, 0);
+  uint32_t pos = a, neg = 0;
+  if (A) { if (lf) neg += __vmaxu2(a, P(0, -1)); } else if (rt) neg += __vmaxu2(a, P(0, 1));          // e_x
+  if (B) { if (up) neg += __vmaxu2(a, P(-1, 0)); } else if (dn) neg += __vmaxu2(a, P(1, 0));          // e_y
+  if (C) { if (up && lf) neg += __vmaxu2(a, P(-1, -1)); } else if (dn && rt) neg += __vmaxu2(a, P(1, 1));  // e_diag
+  if (B && C) { if (up && lf) pos += __vmaxu2(__vmaxu2(a, P(-1, -1)), P(-1, 0)); }                  // U
+  else if (A && !B) { if (lf && dn) pos += __vmaxu2(__vmaxu2(a, P(0, -1)), P(1, 0)); }
+  else if (rt && dn) pos += __vmaxu2(__vmaxu2(a, P(0, 1)), P(1, 1));
+  if (A && C) { if (up && lf) pos += __vmaxu2(__vmaxu2(a, P(-1, -1)), P(0, -1)); }                  // L
+  else if (B && !A) { if (up && rt) pos += __vmaxu2(__vmaxu2(a, P(-1, 0)), P(0, 1)); }
+  else if (dn && rt) pos += __vmaxu2(__vmaxu2(a, P(1, 0)), P(1, 1));
+  return pos - neg;
+}
+
+template <typename OutT, bool FREUD>
 __global__ void __launch_bounds__(kSweepWarps * 32, 1)
     k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint32_t* __restrict__ prog,
               const int* __restrict__ prog_len, const int* __restrict__ qlist, const int* __restrict__ qcount,
@@ -349,7 +414,6 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   int* st = (int*)wbase;                                             // [kStageBins][kStageStride]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lane4 = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
-  const int qc0 = qcount[0], qc1 = qcount[1], qc2 = qcount[2], qc3 = qcount[3];
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
   if (threadIdx.x < 32) cwb[HW * 32 + threadIdx.x] = 0u;  // padding row: weight 0
 
@@ -377,12 +441,22 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       }
     }
 #pragma unroll 1
-    for (int o = 0; o < 4; ++o) {
-      const int qco = o == 0 ? qc0 : (o == 1 ? qc1 : (o == 2 ? qc2 : qc3));
+    for (int o = 0; o < (FREUD ? 8 : 4); ++o) {
+      const int qco = qcount[o];
       if (qco == 0) continue;
       __syncthreads();  // pix staged / previous quadrant's sweeps done with cwb
       const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
-      {
+      if (FREUD) {
+        int v = threadIdx.x >> 5;
+        int r = v / W, c = v - r * W;
+        const int step_r = kSweepWarps / W, step_c = kSweepWarps - step_r * W;
+        for (; v < HW; v += kSweepWarps) {
+          cwb[v * 32 + lane] = freud_cw(pix + v * kPixStride + 2 * lane, r, c, H, W, o & 1, (o >> 1) & 1, (o >> 2) & 1);
+          r += step_r;
+          c += step_c;
+          if (c >= W) { c -= W; ++r; }
+        }
+      } else {
         // element (v, lane): cw of images 2l, 2l+1 as the signed packed pair
         // cw0 + cw1 * 2^16 (mod 2^32): (a + m_diag) - (m_c + m_r) in plain u32 arithmetic
         // (each operand half <= 510, so the borrow of a negative cw0 lands in cw1's half).
@@ -410,6 +484,34 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
         sweep_direction<OutT>(lane4, prog + (int64_t)dl * Lw, prog_len[dl], Lp, st, out, img0, nimg, Dc, dl, T, lane);
         __syncwarp();
       }
+    }
+  }
+}
+
+// Freudenthal corrections (after k_sweep2d): simplex (dl, u, t) was counted from bin lo but
+// belongs to bin hi > lo: subtract its signed weight from the cumulative bins [lo, hi).
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_sweep_fix(const uint8_t* __restrict__ img, int64_t B, int H, int W,
+                                                   const int4* __restrict__ corr, const int* __restrict__ ncorr,
+                                                   int Dc, int T, OutT* __restrict__ out) {
+  const int64_t n = (int64_t)*ncorr * B;
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / B, b = i - e * B;
+    const int4 c = corr[e];
+    const uint8_t* p = img + b * HW + c.y;
+    const int off[4] = {0, 1, W, W + 1};
+    const int mask = freud_mask(c.z);
+    int mx = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (mask >> k & 1) mx = max(mx, (int)p[off[k]]);
+    const int sw = (c.z >= 4) ? mx : -mx;  // (-1)^dim: edges -1, triangles +1
+    if (sw == 0) continue;
+    OutT* row = out + (b * Dc + c.x) * (int64_t)T;
+    for (int q = c.w & 0xFFFF; q < (c.w >> 16); ++q) {
+      if (sizeof(OutT) == 4) atomicAdd((int*)(row + q), -sw);
+      else atomicAdd((unsigned long long*)(row + q), (unsigned long long)(long long)(-sw));
     }
   }
 }
@@ -630,39 +732,55 @@ bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
 
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc,
                            int T, const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
-                           int num_sms) {
+                           int num_sms, int freud) {
   const int HW = H * W;
   const int Lp = sweep_prog_packets(HW, T);
   uint32_t* prog = (uint32_t*)scratch;
   int* ints = (int*)(((uintptr_t)(prog + (size_t)Dc * sweep_prog_words(HW, T)) + 15) & ~(uintptr_t)15);
-  int* qcount = ints;
-  int* prog_len = ints + 4;
-  int* qlist = prog_len + Dc;
-  WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 4 * sizeof(int), st));
+  int* qcount = ints;           // 8 chamber slots (cubical uses 4)
+  int* prog_len = ints + 8;
+  int* qlist = prog_len + Dc;   // [8][Dc]
+  int* ncorr = qlist + 8 * Dc;
+  int4* corr = (int4*)(((uintptr_t)(ncorr + 1) + 15) & ~(uintptr_t)15);
+  const int corr_cap = freud ? 5 * HW * Dc : 0;
+  WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 8 * sizeof(int), st));
+  WECT_CUDA_TRY(cudaMemsetAsync(ncorr, 0, sizeof(int), st));
   const size_t sort_smem = (size_t)(2 * T + Lp) * sizeof(int) + align16((size_t)HW * 2);
   if (sort_smem > 48 * 1024) WECT_CUDA_TRY(cudaFuncSetAttribute(k_sort2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
-  k_sort2d<<<Dc, 256, sort_smem, st>>>(H, W, dirs, d_begin, Dc, gp, prog, prog_len, qlist, qcount); count_launch();
+  k_sort2d<<<Dc, 256, sort_smem, st>>>(H, W, dirs, d_begin, Dc, gp, prog, prog_len, qlist, qcount, freud, corr, ncorr,
+                                       corr_cap); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   const size_t smem = sweep_smem_bytes(HW, T);
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
   const int grid = (int)(ngroups < num_sms ? ngroups : num_sms);
   MainTimer timer(st);
+#define WECT_SWEEP(OT, FR)                                                                                   \
+  do {                                                                                                       \
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<OT, FR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_sweep2d<OT, FR><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, prog, prog_len, qlist, qcount, Dc, T,  \
+                                                             (OT*)out);                                         \
+    count_launch();                                                                                          \
+  } while (0)
   if (odtype == WECT_I32) {
-    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_sweep2d<int32_t><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, prog, prog_len, qlist, qcount, Dc, T,
-                                                             (int32_t*)out); count_launch();
+    if (freud) WECT_SWEEP(int32_t, true); else WECT_SWEEP(int32_t, false);
   } else {
-    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_sweep2d<long long><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, prog, prog_len, qlist, qcount, Dc, T,
-                                                               (long long*)out); count_launch();
+    if (freud) WECT_SWEEP(long long, true); else WECT_SWEEP(long long, false);
   }
+#undef WECT_SWEEP
   timer.stop();
+  if (freud) {  // the rare rounded-diagonal simplices (usually none)
+    const int fb = num_sms * 4;
+    if (odtype == WECT_I32) k_sweep_fix<int32_t><<<fb, 256, 0, st>>>(img, B, H, W, corr, ncorr, Dc, T, (int32_t*)out);
+    else k_sweep_fix<long long><<<fb, 256, 0, st>>>(img, B, H, W, corr, ncorr, Dc, T, (long long*)out);
+    count_launch();
+  }
   WECT_CUDA_TRY(cudaGetLastError());
   return WECT_OK;
 }
 
-size_t sweep2d_scratch_bytes(int HW, int Dc, int T) {
-  return (size_t)Dc * sweep_prog_words(HW, T) * 4 + 16 + (size_t)(4 + Dc + 4 * Dc) * 4 + 64;
+size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud) {
+  return (size_t)Dc * sweep_prog_words(HW, T) * 4 + 16 + (size_t)(8 + Dc + 8 * Dc + 1) * 4 + 64 +
+         (freud ? (size_t)5 * HW * Dc * sizeof(int4) + 16 : 0);
 }
 
 // histogram path over a chunk of images [b0, b0 + nb): cwo scratch for nb images, diff rows at b0

@@ -69,3 +69,30 @@ def test_freudenthal_mnist_batch_sampled():
     idx = np.sort(np.random.default_rng(13).choice(img.shape[0], 24, replace=False))
     ref = oracle.wect_images_freudenthal(img[idx], dirs, T)
     assert (out[torch.from_numpy(idx).to(DEV)].cpu().numpy() == ref).all()
+
+
+def test_freudenthal_sweep_near_antidiagonal_directions():
+    """Directions with s_x + s_y ~ 0 (the chamber wall of the diagonal): the sweep's chamber
+    regrouping needs its exact correction list there (rounded diagonal comparisons); the
+    histogram path (WECT_FREUD_HIST-free shapes > 1023 pixels) needs none."""
+    base = np.array([[-0.70710677, 0.70710677], [0.70710677, -0.70710677]], np.float32)
+    eps = [0.0, 1e-7, -1e-7, 3e-6, -3e-6, 1e-4]
+    dirs = np.concatenate([base + np.array([0.0, e], np.float32) for e in eps] + [synth.directions_s1(16)])
+    dirs = dirs.astype(np.float32)
+    for H, W, T in [(28, 28, 128), (13, 17, 255), (31, 33, 64)]:
+        img = synth.images_u8(20, (H, W), 950 + H)
+        assert (gpu(img, dirs, T) == oracle.wect_images_freudenthal(img, dirs, T)).all(), (H, W, T)
+
+
+def test_freudenthal_sweep_correction_list_is_exercised():
+    """A direction found by search (CPU, oracle binary64 bins) for which two diagonal pairs of
+    a 20x24 grid at T = 1000 have their rounded height order opposite to the chamber of
+    s_x + s_y, with a bin edge in between: the sweep must apply its correction list."""
+    dirs = np.array([[0.8697633743286133, -0.8697633147239685], [0.6, 0.8], [-0.8, 0.6]], np.float32)
+    fv = oracle.heights(oracle.grid_coords((20, 24)), dirs[:1])[:, 0]
+    M = np.abs(oracle.heights(oracle.grid_coords((20, 24)), dirs)).max()
+    vb = oracle.alpha_vec(fv, -M, M, 1000).reshape(20, 24)
+    assert (vb[1:, 1:] < vb[:-1, :-1]).any()  # the designated (upper-right) vertex has the lower bin
+    img = synth.images_u8(30, (20, 24), 977)
+    img[:, :, :] = np.maximum(img, 1)  # every simplex weight non-zero
+    assert (gpu(img, dirs, 1000) == oracle.wect_images_freudenthal(img, dirs, 1000)).all()
