@@ -231,13 +231,14 @@ def alpha_vec(t: np.ndarray, lo: float, hi: float, T: int) -> np.ndarray:
     return np.clip(np.ceil(u), 0, T - 1).astype(np.int64)
 
 
-def wecfs_grad(fvals: np.ndarray, cx, T: int, lo: float, hi: float, G: np.ndarray):
+def wecfs_grad(fvals: np.ndarray, cx, T: int, lo: float, hi: float, G: np.ndarray, vertices=None):
     """dL/dw for L with G = dL/dWECFs [m, T], straight from the closed form:
     WECFs[p, q] = sum_s w(s) (-1)^dim s [bin(s, p) <= q], bin(s, p) = max over the vertices
     of s of alpha(f_p(v)) (Alg. 1 lines 3, 7-8), so
         dL/dw(s) = sum_{p, q} G[p, q] (-1)^dim s [bin(s, p) <= q].
-    The indicator is materialised ([cells, m, T]) -- small inputs only.
-    Returns (grad_vweights [k0], [grad_cells_i]) in float64."""
+    The indicator is materialised ([cells, m, T]) -- small inputs only (`vertices`: an index
+    subset for the vertex part, e.g. samples of a full-size complex).
+    Returns (grad_vweights [k0] or [len(vertices)], [grad_cells_i]) in float64."""
     fv = np.asarray(fvals, np.float64)
     G = np.asarray(G, np.float64)
     vb = alpha_vec(fv, lo, hi, T)  # [k0, m]
@@ -247,7 +248,7 @@ def wecfs_grad(fvals: np.ndarray, cx, T: int, lo: float, hi: float, G: np.ndarra
         ind = (bins[:, :, None] <= q[None, None, :]).astype(np.float64)
         return sign * np.einsum("spq,pq->s", ind, G)
 
-    gv = grad_of(vb, 1.0)
+    gv = grad_of(vb if vertices is None else vb[np.asarray(vertices)], 1.0)
     gc = []
     for c in cx.cells:
         v = np.asarray(c.verts, np.int64).reshape(len(c.verts), -1)

@@ -155,3 +155,34 @@ def test_backward_edge_cases_and_errors():
     assert (gv.numpy() == 7.0).all()
     for (v, _, d), g in zip(cells, gc):
         assert (g.numpy() == (7.0 if d % 2 == 0 else -7.0)).all()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("c", [3, 4])
+def test_backward_full_size_sampled_vs_oracle(c):
+    """bwd3 / bwd4 at BASELINE's full sizes (cfg4 mesh, D = 1024, T = 512; cfg5 complex,
+    D = 256, T = 256) in the bench launch configuration; the oracle's closed form on 64
+    sampled cells of every dimension and 64 sampled vertices, M over ALL directions (A2)."""
+    d = synth.make_config(c)
+    cx, dirs, T = d["complex"], d["dirs"], d["T"]
+    D = dirs.shape[0]
+    G = synth.rng(synth.S0 + 70 + c).integers(-3, 4, size=(D, T)).astype(np.float64)
+    gv, gc = w.wect_complex_backward(torch.from_numpy(cx.coords).to(DEV), _cells(cx), torch.from_numpy(dirs).to(DEV), T,
+                                     torch.from_numpy(G).to(DEV))
+    w.sync_status()
+    g = np.random.default_rng(100 + c)
+    M = 0.0  # M over ALL vertices and directions (A2), chunked over directions
+    for a in range(0, D, 64):
+        M = max(M, float(np.abs(oracle.heights(cx.coords, dirs[a:a + 64])).max()))
+    vs = np.sort(g.choice(cx.k0, 64, replace=False))
+    picks = [np.sort(g.choice(len(x.verts), 64, replace=False)) for x in cx.cells]
+    # heights of the vertices the samples touch only, ids remapped into that subset
+    need = np.unique(np.concatenate([vs] + [x.verts[i].reshape(-1) for x, i in zip(cx.cells, picks)]))
+    remap = {int(v): k for k, v in enumerate(need)}
+    fv = oracle.heights(np.ascontiguousarray(cx.coords[need]), dirs)
+    sub = synth.Complex(None, None, [synth.Cells(np.vectorize(remap.get)(x.verts[i]).astype(np.int32), None, x.dim)
+                                     for x, i in zip(cx.cells, picks)], len(need))
+    ov, oc = oracle.wecfs_grad(fv, sub, T, -M, M, G, vertices=[remap[int(v)] for v in vs])
+    assert (gv[torch.from_numpy(vs).to(DEV)].cpu().numpy() == ov).all()
+    for gi, i, o in zip(gc, picks, oc):
+        assert (gi[torch.from_numpy(i).to(DEV)].cpu().numpy() == o).all()
