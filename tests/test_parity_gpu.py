@@ -475,3 +475,16 @@ def test_ecf_single_filter_integer_weights_vs_O2():
     out = w.ecf_complex(torch.from_numpy(fi).to(DEV), cells_of(cx), 256, vweights=torch.from_numpy(cx.vweights).to(DEV),
                         lo=0.0, hi=255.0).cpu().numpy()
     assert (out == oracle.ecf_complex(cx, fi, 256, lo=0.0, hi=255.0)).all()
+
+
+@pytest.mark.slow
+def test_ecfx_full_size_vs_O2():
+    """The ECF-X bench workload at full size (cfg4 mesh, one filter U[-1,1], T = 512, integer
+    weights) in the bench launch configuration: the whole row against O2, bit-exact."""
+    c = synth.make_config(3)
+    cx = c["complex"]
+    f = synth.rng(synth.S0 + 60).uniform(-1, 1, (cx.k0, 1)).astype(np.float32)
+    out = w.ecf_complex(torch.from_numpy(f).to(DEV), cells_of(cx), 512,
+                        vweights=torch.from_numpy(cx.vweights).to(DEV)).cpu().numpy()
+    w.sync_status()
+    assert (out == oracle.ecf_complex(cx, f, 512)).all()
