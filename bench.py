@@ -309,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
     per_call_launches = tl / max(K, 1)  # timed (dominant-kernel) launches per step
     D = wl["dirs"].shape[0] if "dirs" in wl else 1
     if wl["kind"] == "ecfimg":
-        kname, bound = ("k_ecf_img2d_w4", "hbm") if args.config == "ecfimg" else ("k_ecf_img_hist", "alu")
+        kname, bound = ("k_ecf_img2d_w4", "hbm") if args.config == "ecfimg" else ("k_ecf_img2d_rows", "alu")
     elif wl["kind"] == "images" and (args.config in ("0", "1") or wl.get("freudenthal")):
         kname, bound = "k_sweep2d", "hbm"
     elif wl["kind"] == "images":

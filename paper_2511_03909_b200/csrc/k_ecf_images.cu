@@ -30,6 +30,7 @@
 // Larger images: CTAs over vertex chunks add their histograms into an int64 [B][256]
 // table (plus the per-image max), then one warp per image scans and maps.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -385,6 +386,84 @@ __global__ void __launch_bounds__(256) k_ecf_img_hist(const uint8_t* __restrict_
   if (threadIdx.x == 0) atomicMax(gmax + b, smax);
 }
 
+// Large 2-D images with W % 4 == 0: the packed u16x2 anchor step of k_ecf_img2d_w4 over a
+// block of kEcfRows rows per CTA (plus the next row as halo; a sink row below the last),
+// staged in shared memory with coalesced 4-byte loads; per-warp histograms merged into the
+// int64 [B][256] table, the block's max intensity into gmax.
+constexpr int kEcfRows = 16;
+
+__global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img2d_rows(const uint8_t* __restrict__ img, int H, int W,
+                                                                   unsigned long long* __restrict__ ghist,
+                                                                   unsigned int* __restrict__ gmax) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P2 = (W + 2) >> 1, W2 = W >> 1, W4 = W >> 2;
+  const int64_t b = blockIdx.y;
+  const int r0 = blockIdx.x * kEcfRows;
+  const int R = (H - r0) < kEcfRows ? (H - r0) : kEcfRows;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
+  unsigned char* hbase = smem + (((s0 + 2047u) & ~2047u) - s0);
+  int* hist = (int*)(hbase + (size_t)warp * 2048);
+  uint32_t* S = (uint32_t*)(hbase + kEcfWarps * 2048);  // [(R + 1)][P2] words
+  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(hist);
+  __shared__ unsigned int smax;
+  if (threadIdx.x == 0) smax = 0;
+  for (int k = lane; k < 256; k += 32) hist[k] = 0;
+  // stage rows r0 .. r0 + R (the last one the halo, or the sink row below the image)
+  const uint32_t* src = (const uint32_t*)(img + (b * H + r0) * (int64_t)W);
+  unsigned mx = 0;
+  for (int i = threadIdx.x; i < (R + 1) * W4; i += blockDim.x) {
+    const int rr = i / W4, q = i - rr * W4;
+    uint32_t lo = (uint32_t)kSinkOff | ((uint32_t)kSinkOff << 16), hi = lo;
+    if (r0 + rr < H) {
+      const uint32_t wv = __ldcs(src + (int64_t)rr * W4 + q);
+      lo = __byte_perm(wv, 0, 0x4140) << 2;
+      hi = __byte_perm(wv, 0, 0x4342) << 2;
+      if (rr < R) mx = __vmaxu4(mx, wv);
+    }
+    S[rr * P2 + 2 * q] = lo;
+    S[rr * P2 + 2 * q + 1] = hi;
+  }
+  for (int rr = threadIdx.x; rr < R + 1; rr += blockDim.x)  // the padding column of every row
+    S[rr * P2 + W2] = (uint32_t)kSinkOff | ((uint32_t)kSinkOff << 16);
+  mx = max(max(mx & 0xFFu, (mx >> 8) & 0xFFu), max((mx >> 16) & 0xFFu, mx >> 24));
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  __syncthreads();
+  if (lane == 0) atomicMax(&smax, mx);
+  const int nitems = R * W2;
+  for (int it = warp * 32 + lane; it < nitems; it += blockDim.x) {
+    const int r = it / W2, xp = it - r * W2;
+    const int ai = r * P2 + xp;
+    const uint32_t a2 = S[ai], an = S[ai + 1], c2 = S[ai + P2], cn = S[ai + P2 + 1];
+    const uint32_t b2 = __byte_perm(a2, an, 0x5432), d2 = __byte_perm(c2, cn, 0x5432);
+    const uint32_t m_x = __vmaxu2(a2, b2), m_y = __vmaxu2(a2, c2);
+    const uint32_t m_xy = __vmaxu2(m_x, __vmaxu2(c2, d2));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t A = (h ? a2 >> 16 : a2 & 0xFFFFu) | wbase;
+      const uint32_t X = (h ? m_x >> 16 : m_x & 0xFFFFu) | wbase;
+      const uint32_t Y = (h ? m_y >> 16 : m_y & 0xFFFFu) | wbase;
+      const uint32_t XY = (h ? m_xy >> 16 : m_xy & 0xFFFFu) | wbase;
+      if (X != A) {
+        asm volatile("red.shared.add.s32 [%0], 1;" ::"r"(A) : "memory");
+        asm volatile("red.shared.add.s32 [%0], -1;" ::"r"(X) : "memory");
+      }
+      if (XY != Y) {
+        asm volatile("red.shared.add.s32 [%0], -1;" ::"r"(Y) : "memory");
+        asm volatile("red.shared.add.s32 [%0], 1;" ::"r"(XY) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+    int sum = 0;
+#pragma unroll
+    for (int w8 = 0; w8 < kEcfWarps; ++w8) sum += ((const int*)(hbase + (size_t)w8 * 2048))[c];
+    if (sum != 0) atomicAdd(ghist + b * 256 + c, (unsigned long long)(long long)sum);
+  }
+  if (threadIdx.x == 0) atomicMax(gmax + b, smax);
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(kEcfWarps * 32) k_ecf_img_final(const unsigned long long* __restrict__ ghist,
                                                                   const unsigned int* __restrict__ gmax, int64_t B,
@@ -459,8 +538,18 @@ static wect_status launch_ecf_images_t(const uint8_t* img, int64_t B, int ndim, 
   unsigned long long* ghist = (unsigned long long*)((char*)scratch + off);
   unsigned int* gmax = (unsigned int*)(ghist + (size_t)B * 256);
   WECT_CUDA_TRY(cudaMemsetAsync(ghist, 0, (size_t)B * 256 * 8 + (size_t)B * 4, st));
-  dim3 g((unsigned)((nv + kEcfChunk - 1) / kEcfChunk), (unsigned)B);
-  {
+  const bool rows_path = ndim == 2 && X % 4 == 0 && X <= 16384 && ((uintptr_t)img & 3) == 0 &&
+                         !getenv("WECT_ECF_GENERIC");
+  if (rows_path) {
+    const size_t smem = 2048 + (size_t)kEcfWarps * 2048 + (size_t)(kEcfRows + 1) * ((X + 2) >> 1) * 4;
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf_img2d_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 g((unsigned)((Y + kEcfRows - 1) / kEcfRows), (unsigned)B);
+    MainTimer timer(st);
+    k_ecf_img2d_rows<<<g, kEcfWarps * 32, smem, st>>>(img, Y, X, ghist, gmax);
+    count_launch();
+    timer.stop();
+  } else {
+    dim3 g((unsigned)((nv + kEcfChunk - 1) / kEcfChunk), (unsigned)B);
     MainTimer timer(st);
     if (ndim == 2) k_ecf_img_hist<2><<<g, 256, 0, st>>>(img, X, Y, 1, ghist, gmax);
     else k_ecf_img_hist<3><<<g, 256, 0, st>>>(img, X, Y, Z, ghist, gmax);

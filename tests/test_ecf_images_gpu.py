@@ -116,3 +116,17 @@ def test_ecf_images_errors_and_row_args():
     g = L.wect_grid(8, 0, 0, 0.0, 0.0, 0.0, 0)
     st = L.load().ecf_images(zero.data_ptr(), 2, 4, dims, ctypes.byref(g), out.data_ptr(), L.I32, None)  # ndim 4
     assert st == L.EINVAL
+
+
+@pytest.mark.parametrize("dims,B", [((100, 4), 3), ((65, 132), 2), ((16, 400), 2), ((17, 300), 3)])
+def test_ecf_images_large_row_block_path(dims, B):
+    """Large 2-D images with W % 4 == 0 take the row-block kernel (16 rows + halo per CTA):
+    row counts not a multiple of 16, W = 4, both grids; a 1-byte-misaligned input takes the
+    generic large-image kernel."""
+    img = synth.images_u8(B, dims, 1200 + dims[0] + dims[1])
+    for g in (dict(), dict(lo=0.0, hi=255.0)):
+        assert (gpu(img, 256, **g) == _orc(img, 256, g)).all()
+    raw = torch.zeros(img.size + 1, dtype=torch.uint8, device=DEV)
+    raw[1:] = torch.from_numpy(img.reshape(-1)).to(DEV)
+    out = w.ecf_images(raw[1:].view(img.shape), 64).cpu().numpy()
+    assert (out == _orc(img, 64, dict())).all()
