@@ -316,6 +316,7 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
   const bool fast = sizeof(OutT) == 4 && nimg == kSweepImgs && (T % kStageBins) == 0;
   OutT* const lp = out + ((img0 + (lane >> 1)) * Dc + dl) * (int64_t)T + 4 * (lane & 1);
   const int64_t rstride = (int64_t)16 * Dc * T;
+  int* const stl = st + 2 * lane;  // this lane's column pair of the stage
   // the program streams from L2: prefetch it into L1 (one 128-byte line per lane)
   if (lane * 8 < npk) asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + lane * 8));
   if (lane * 32 < npk / 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(metaw + lane * 32));
@@ -339,30 +340,34 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane4, const uint32_t* 
       mw = __ldg(metaw + (k >> 2) + 1);
     }
     if (m & 0xFEFEFEFEu) {  // some packet of the group ends a bin
+      // one emitted bin: stage the running totals, flush a full 8-bin chunk
+      auto emit = [&](const int2 v) {
+        *(int2*)(stl + (q & (kStageBins - 1)) * kStageStride) = v;
+        if (((++q) & (kStageBins - 1)) == 0) {
+          __syncwarp();
+          if (fast) {  // full group, int32, whole chunks: unguarded 16-byte stores
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int mm = r * 16 + (lane >> 1), j4 = 4 * (lane & 1);
+              const int4 x = make_int4(st[(j4 + 0) * kStageStride + mm], st[(j4 + 1) * kStageStride + mm],
+                                       st[(j4 + 2) * kStageStride + mm], st[(j4 + 3) * kStageStride + mm]);
+              __stcs((int4*)(lp + r * rstride + (q - kStageBins)), x);
+            }
+          } else {
+            sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q - kStageBins, lane);
+          }
+          __syncwarp();
+        }
+      };
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        int e = (int)((m >> (8 * j + 1)) & 0x7Fu);
-        if (e) {
-          const int2 s = unpack_s16x2(P[j]);
-          const int2 v = make_int2(base0 + s.x, base1 + s.y);
-          for (; e > 0; --e) {
-            *(int2*)(st + (q & (kStageBins - 1)) * kStageStride + 2 * lane) = v;
-            if (((++q) & (kStageBins - 1)) == 0) {
-              __syncwarp();
-              if (fast) {  // full group, int32, whole chunks: unguarded 16-byte stores
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                  const int mm = r * 16 + (lane >> 1), j4 = 4 * (lane & 1);
-                  const int4 x = make_int4(st[(j4 + 0) * kStageStride + mm], st[(j4 + 1) * kStageStride + mm],
-                                           st[(j4 + 2) * kStageStride + mm], st[(j4 + 3) * kStageStride + mm]);
-                  __stcs((int4*)(lp + r * rstride + (q - kStageBins)), x);
-                }
-              } else {
-                sweep_store_chunk<OutT>(st, out, img0, nimg, Dc, dl, T, q - kStageBins, lane);
-              }
-              __syncwarp();
-            }
-          }
+        const uint32_t mj = m & (0xFEu << (8 * j));  // emit count of packet j, in place
+        if (mj) {
+          const int2 sv = unpack_s16x2(P[j]);
+          const int2 v = make_int2(base0 + sv.x, base1 + sv.y);
+          emit(v);
+          if (__builtin_expect(mj > (2u << (8 * j)), 0))  // empty bins after it: same total
+            for (int e = (int)(mj >> (8 * j + 1)) - 1; e > 0; --e) emit(v);
         }
       }
     }
