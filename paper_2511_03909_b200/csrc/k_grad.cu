@@ -17,6 +17,7 @@
 // cell c's sum over the 32 filters.  Tiles add into the fp64 gradient in a fixed order, so the
 // result is deterministic.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -70,7 +71,7 @@ __device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) 
 
 // One pass: filters [row0, row0 + np) of the tile (np <= 32), lane = filter; batches of
 // 16 cells, 8 cells x AR VB loads in flight at a time (AR = 0: runtime arity <= 8).
-template <bool SMEM_RC, int AR>
+template <bool SMEM_RC, bool PAIR, int AR>
 __device__ __forceinline__ void grad_segment(const Seg& S, double* __restrict__ go, int64_t k0,
                                              const uint16_t* __restrict__ vb16, int np, const double* __restrict__ rcs,
                                              const double* __restrict__ RC, int row0, int T, int first, int64_t gw,
@@ -105,16 +106,25 @@ __device__ __forceinline__ void grad_segment(const Seg& S, double* __restrict__ 
           if (AR == 0 && j >= ar) { b[c][j] = 0; continue; }
           const int id = __shfl_sync(0xffffffffu, ids[j], c0 + c);
           ok[c] &= id >= 0;
-          b[c][j] = __ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64);
+          // PAIR: the lane's two directions (2 lane, 2 lane + 1) as one u16x2 word of the row
+          b[c][j] = PAIR ? (int)__ldg((const uint32_t*)vb16 + (int64_t)(id < 0 ? 0 : id) * 32)
+                         : (int)__ldg(vb16 + (int64_t)(id < 0 ? 0 : id) * 64);
         }
       }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        int bin = b[c][0];
-#pragma unroll
-        for (int j = 1; j < MA; ++j) bin = max(bin, b[c][j]);
         double x = 0.0;
-        if (ok[c] && lane < np) x = SMEM_RC ? rcs[bin * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bin);
+        if (PAIR) {  // SMEM_RC is implied: rcs[q][half][32]
+          uint32_t m2 = (uint32_t)b[c][0];
+#pragma unroll
+          for (int j = 1; j < MA; ++j) m2 = __vmaxu2(m2, (uint32_t)b[c][j]);
+          if (ok[c]) x = rcs[(m2 & 0xFFFFu) * 64 + lane] + rcs[(m2 >> 16) * 64 + 32 + lane];
+        } else {
+          int bin = b[c][0];
+#pragma unroll
+          for (int j = 1; j < MA; ++j) bin = max(bin, b[c][j]);
+          if (ok[c] && lane < np) x = SMEM_RC ? rcs[bin * 32 + lane] : __ldg(RC + (int64_t)(row0 + lane) * T + bin);
+        }
         v[c0 + c] = x;
       }
     }
@@ -127,20 +137,28 @@ __device__ __forceinline__ void grad_segment(const Seg& S, double* __restrict__ 
   }
 }
 
-template <bool SMEM_RC>
+// PAIR (T small enough for a [T][2][32] fp64 tile): one pass per 64-filter tile, lane =
+// filters (2 lane, 2 lane + 1); otherwise two passes of 32 (half), lane = filter.
+template <bool SMEM_RC, bool PAIR>
 __global__ void __launch_bounds__(kGradWarps * 32, 1) k_grad_cells(Segs segs, int64_t k0, const uint32_t* __restrict__ vb,
                                                                    int half, int np, const double* __restrict__ RC,
                                                                    int row0, int T, GradOut gout, int first) {
-  extern __shared__ __align__(16) double rcs[];  // [T][32]
+  extern __shared__ __align__(16) double rcs[];  // [T][32], PAIR: [T][2][32] (column half * 32 + l = filter 2 l + half)
   const int lane = threadIdx.x & 31;
-  if (SMEM_RC) {
+  if (PAIR) {
+    for (int i = threadIdx.x; i < T * 64; i += blockDim.x) {
+      const int q = i >> 6, col = i & 63, f = 2 * (col & 31) + (col >> 5);
+      rcs[i] = f < np ? RC[(int64_t)(row0 + f) * T + q] : 0.0;
+    }
+    __syncthreads();
+  } else if (SMEM_RC) {
     for (int i = threadIdx.x; i < T * 32; i += blockDim.x) {
       const int q = i >> 5, l = i & 31;
       rcs[i] = l < np ? RC[(int64_t)(row0 + l) * T + q] : 0.0;
     }
     __syncthreads();
   }
-  const uint16_t* vb16 = (const uint16_t*)vb + half * 32 + lane;
+  const uint16_t* vb16 = PAIR ? (const uint16_t*)(vb + lane) : (const uint16_t*)vb + half * 32 + lane;
   const int64_t gw = (int64_t)blockIdx.x * kGradWarps + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * kGradWarps;
   for (int si = 0; si < segs.nseg; ++si) {
@@ -148,11 +166,11 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1) k_grad_cells(Segs segs, in
     double* go = gout.g[si];
     if (!go || S.count == 0) continue;
     switch (S.arity) {
-      case 1: grad_segment<SMEM_RC, 1>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
-      case 2: grad_segment<SMEM_RC, 2>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
-      case 3: grad_segment<SMEM_RC, 3>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
-      case 4: grad_segment<SMEM_RC, 4>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
-      default: grad_segment<SMEM_RC, 0>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 1: grad_segment<SMEM_RC, PAIR, 1>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 2: grad_segment<SMEM_RC, PAIR, 2>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 3: grad_segment<SMEM_RC, PAIR, 3>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      case 4: grad_segment<SMEM_RC, PAIR, 4>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
+      default: grad_segment<SMEM_RC, PAIR, 0>(S, go, k0, vb16, np, rcs, RC, row0, T, first, gw, nwarps, lane); break;
     }
   }
 }
@@ -174,13 +192,17 @@ wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* 
   WECT_CUDA_TRY(cudaGetLastError());
   const size_t smem = (size_t)T * 32 * sizeof(double);
   const bool use_smem = smem <= 160 * 1024;
-  if (use_smem) {
-    WECT_CUDA_TRY(cudaFuncSetAttribute(k_grad_cells<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool pair = 2 * smem <= 160 * 1024 && !getenv("WECT_GRAD_NOPAIR");
+  if (pair) {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_grad_cells<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * smem)));
+  } else if (use_smem) {
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_grad_cells<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   int64_t maxc = 0;
   for (int i = 0; i < segs.nseg; ++i) maxc = segs.s[i].count > maxc ? segs.s[i].count : maxc;
   int64_t want = (maxc + 16 * kGradWarps - 1) / (16 * kGradWarps);
-  const int per_sm = use_smem ? (int)((200 * 1024) / smem > 2 ? 2 : ((200 * 1024) / smem < 1 ? 1 : (200 * 1024) / smem)) : 2;
+  const size_t esm = pair ? 2 * smem : smem;
+  const int per_sm = use_smem ? (int)((200 * 1024) / esm > 2 ? 2 : ((200 * 1024) / esm < 1 ? 1 : (200 * 1024) / esm)) : 2;
   const int ctas = (int)(want < (int64_t)num_sms * per_sm ? (want < 1 ? 1 : want) : (int64_t)num_sms * per_sm);
   wect_status s = WECT_OK;
   for (int t0 = 0; t0 < Dc && s == WECT_OK; t0 += 64) {
@@ -193,16 +215,26 @@ wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* 
       vblocks = vblocks > num_sms * 16 ? num_sms * 16 : (vblocks < 1 ? 1 : vblocks);
       k_vbins_f<<<vblocks, 256, 0, st>>>(fsrc, k0, m_or_D, d_begin + t0, np, gp, vb); count_launch();
     }
+    if (pair) {
+      MainTimer timer(st);
+      k_grad_cells<true, true><<<ctas, kGradWarps * 32, 2 * smem, st>>>(segs, k0, vb, 0, np, RC, t0, T, gout,
+                                                                         t0 == 0 ? 1 : 0);
+      count_launch();
+      timer.stop();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) s = fail_cuda(e, "k_grad_cells", __FILE__, __LINE__);
+      continue;
+    }
     for (int half = 0; half < 2; ++half) {
       const int nph = np - 32 * half;
       if (nph <= 0) break;
       const int first = (t0 == 0 && half == 0) ? 1 : 0;
       MainTimer timer(st);
       if (use_smem)
-        k_grad_cells<true><<<ctas, kGradWarps * 32, smem, st>>>(segs, k0, vb, half, nph < 32 ? nph : 32, RC,
+        k_grad_cells<true, false><<<ctas, kGradWarps * 32, smem, st>>>(segs, k0, vb, half, nph < 32 ? nph : 32, RC,
                                                                t0 + 32 * half, T, gout, first);
       else
-        k_grad_cells<false><<<ctas, kGradWarps * 32, 0, st>>>(segs, k0, vb, half, nph < 32 ? nph : 32, RC,
+        k_grad_cells<false, false><<<ctas, kGradWarps * 32, 0, st>>>(segs, k0, vb, half, nph < 32 ? nph : 32, RC,
                                                              t0 + 32 * half, T, gout, first);
       count_launch();
       timer.stop();
