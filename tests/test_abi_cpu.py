@@ -17,8 +17,9 @@ def _declared():
 
 def test_header_declares_the_boundary():
     names = _declared()
-    for n in ("wect_complex", "wect_images", "ecf_complex", "wect_maxheight", "wect_sync_status", "wect_last_error",
-              "wect_repair_count", "wect_abi_version"):
+    for n in ("wect_complex", "wect_images", "ecf_complex", "ecf_images", "wect_complex_backward",
+              "ecf_complex_backward", "wect_maxheight", "wect_sync_status", "wect_last_error", "wect_repair_count",
+              "wect_abi_version"):
         assert n in names
 
 
@@ -75,3 +76,35 @@ def test_argument_errors_are_synchronous():
     with pytest.raises(w.WectError) as e:
         w.wect_complex(np.zeros((3, 9), np.float32), cells, np.zeros((2, 9), np.float32), 8)  # n = 9 > 8
     assert e.value.status == _lib.EINVAL
+
+
+def test_new_entry_points_reject_bad_arguments_synchronously():
+    """ecf_images and the backward calls validate before touching a device (no GPU here)."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2511_03909_b200 import _lib
+
+    L = _lib.load()
+    img = np.zeros((1, 4, 4), np.uint8)
+    out = np.zeros((1, 8), np.int32)
+    dims = (ctypes.c_int64 * 2)(4, 4)
+    g = _lib.wect_grid(1, 0, 0, 0.0, 0.0, 0.0, 0)  # T < 2
+    assert L.ecf_images(img.ctypes.data, 1, 2, dims, ctypes.byref(g), out.ctypes.data, _lib.I32, None) == _lib.EINVAL
+    g = _lib.wect_grid(8, 0, 0, 0.0, 0.0, 0.0, 0)
+    assert L.ecf_images(img.ctypes.data, 1, 5, dims, ctypes.byref(g), out.ctypes.data, _lib.I32, None) == _lib.EINVAL
+    assert L.ecf_images(img.ctypes.data, 1, 2, dims, ctypes.byref(g), out.ctypes.data, _lib.F64, None) == _lib.EINVAL
+    # wect_complex_backward: NULL complex, T < 2
+    G = np.zeros((2, 8))
+    gv = np.zeros(4)
+    assert L.wect_complex_backward(None, None, 2, ctypes.byref(g), G.ctypes.data, gv.ctypes.data, None,
+                                   None) == _lib.EINVAL
+    # Freudenthal volumes are not supported (a synchronous ENOTSUP)
+    vol = np.zeros((1, 3, 3, 3), np.uint8)
+    d3 = (ctypes.c_int64 * 3)(3, 3, 3)
+    dirs = np.zeros((2, 3), np.float32)
+    o3 = np.zeros((1, 2, 8), np.int32)
+    gf = _lib.wect_grid(8, 0, 0, 0.0, 0.0, 0.0, _lib.FREUDENTHAL)
+    assert L.wect_images(vol.ctypes.data, 1, 3, d3, dirs.ctypes.data, 2, ctypes.byref(gf), o3.ctypes.data, _lib.I32,
+                         None) == _lib.ENOTSUP
