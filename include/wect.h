@@ -170,7 +170,8 @@ WECT_API wect_status ecf_complex(const wect_complex_desc* K, const float* fvals,
  * img: [B, dims...] uint8.  dims: HOST array.  grid->d_begin must be 0 and grid->d_count
  * 0 or 1 (one filter per image); flags other than WECT_TIME_MAIN are ignored.
  * out: [B, T] of WECT_I32 (refused with WECT_EOVERFLOW when #cells >= 2^31) or WECT_I64.
- * T in [2, 65536] (WECT_ENOTSUP above).  Errors as for wect_images. */
+ * T in [2, 65536]; image sides <= 65535; B <= 65535 for images of more than 4096 pixels
+ * (WECT_ENOTSUP otherwise).  Errors as for wect_images. */
 WECT_API wect_status ecf_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_t* dims,
                                 const wect_grid* grid, void* out, wect_dtype odtype, void* stream);
 
@@ -188,7 +189,8 @@ WECT_API wect_status ecf_images(const uint8_t* img, int64_t B, int32_t ndim, con
  * grad_cells: HOST array of K->ncell_dims pointers (or NULL), entry i an [cells[i].count] fp64
  *   output or NULL (skip).  Outputs are overwritten.  Cells of arity > 8: WECT_ENOTSUP.
  * Accumulation: RC = reverse cumsum of each G row in binary64 from q = T-1 down, then the
- *   sum over rows in a fixed order (tiles of 32 rows; a shuffle tree within a tile):
+ *   sum over rows in a fixed order (tiles of 32 rows, or 64 when T <= 320; a shuffle tree
+ *   within a tile):
  *   deterministic, within binary64 rounding of the exact sum (reading A13).
  * Errors as for wect_complex; an out-of-range vertex index is reported by wect_sync_status. */
 WECT_API wect_status wect_complex_backward(const wect_complex_desc* K, const float* dirs, int32_t D,
