@@ -530,22 +530,24 @@ template <int ND>
 __global__ void __launch_bounds__(256) k_grid_cw(const uint8_t* __restrict__ img, int64_t nimg, int64_t d0,
                                                  int64_t d1, int64_t d2, int16_t* __restrict__ cwo) {
   constexpr int NO = 1 << ND;
-  int64_t L[3];  // L[k] = length of axis k (axis 0 fastest)
-  if (ND == 2) { L[0] = d1; L[1] = d0; L[2] = 1; } else { L[0] = d2; L[1] = d1; L[2] = d0; }
-  const int64_t nv = L[0] * L[1] * L[2];
-  const int64_t total = nimg * nv;
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = f / nv, v = f - b * nv;
-    int64_t g[3] = {v % L[0], (v / L[0]) % L[1], v / (L[0] * L[1])};
-    const uint8_t* im = img + b * nv;
+  int L[3];  // L[k] = length of axis k (axis 0 fastest); one image has < 2^31 voxels
+  if (ND == 2) { L[0] = (int)d1; L[1] = (int)d0; L[2] = 1; } else { L[0] = (int)d2; L[1] = (int)d1; L[2] = (int)d0; }
+  const int nv = L[0] * L[1] * L[2];
+  const int L01 = L[0] * L[1];
+  // grid.y walks the images, grid.x x threads the voxels of one image: 32-bit index math
+  for (int64_t b = blockIdx.y; b < nimg; b += gridDim.y)
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const int z0 = v / L01, r01 = v - z0 * L01, y0 = r01 / L[0], x0 = r01 - y0 * L[0];
+    const int g[3] = {x0, y0, z0};
+    const uint8_t* im = img + b * (int64_t)nv;
     // 3^ND neighbourhood, -1 where outside the grid
     int nb[ND == 2 ? 9 : 27];
 #pragma unroll
     for (int t = 0; t < (ND == 2 ? 9 : 27); ++t) {
-      int o0 = t % 3 - 1, o1 = (t / 3) % 3 - 1, o2 = ND == 3 ? t / 9 - 1 : 0;
-      int64_t x = g[0] + o0, y = g[1] + o1, z = g[2] + o2;
-      bool ok = x >= 0 && x < L[0] && y >= 0 && y < L[1] && z >= 0 && z < L[2];
-      nb[t] = ok ? (int)im[(z * L[1] + y) * L[0] + x] : -1;
+      const int o0 = t % 3 - 1, o1 = (t / 3) % 3 - 1, o2 = ND == 3 ? t / 9 - 1 : 0;
+      const int x = g[0] + o0, y = g[1] + o1, z = g[2] + o2;
+      const bool ok = (unsigned)x < (unsigned)L[0] && (unsigned)y < (unsigned)L[1] && (unsigned)z < (unsigned)L[2];
+      nb[t] = ok ? (int)__ldg(im + (z * L[1] + y) * L[0] + x) : -1;
     }
     int16_t res[NO];
 #pragma unroll
@@ -795,9 +797,15 @@ wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndi
   const int64_t nv = ndim == 2 ? dims[0] * dims[1] : dims[0] * dims[1] * dims[2];
   const uint8_t* im = img + b0 * nv;
   const int64_t total = nb * nv;
-  int blocks = (int)((total + 255) / 256 < (int64_t)num_sms * 16 ? (total + 255) / 256 : (int64_t)num_sms * 16);
-  if (ndim == 2) k_grid_cw<2><<<blocks, 256, 0, st>>>(im, nb, dims[0], dims[1], 1, cwo);
-  else k_grid_cw<3><<<blocks, 256, 0, st>>>(im, nb, dims[0], dims[1], dims[2], cwo);
+  (void)total;
+  const int64_t want_x = (nv + 255) / 256;
+  const int gx = (int)(want_x < (int64_t)num_sms * 16 ? want_x : (int64_t)num_sms * 16);
+  int64_t gy = ((int64_t)num_sms * 16 + gx - 1) / gx;
+  gy = gy < nb ? gy : nb;
+  gy = gy < 65535 ? (gy < 1 ? 1 : gy) : 65535;
+  dim3 gcw((unsigned)gx, (unsigned)gy);
+  if (ndim == 2) k_grid_cw<2><<<gcw, 256, 0, st>>>(im, nb, dims[0], dims[1], 1, cwo);
+  else k_grid_cw<3><<<gcw, 256, 0, st>>>(im, nb, dims[0], dims[1], dims[2], cwo);
   count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   const int tiles = (Dc + 31) / 32;
