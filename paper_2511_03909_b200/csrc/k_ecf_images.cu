@@ -367,9 +367,18 @@ __global__ void __launch_bounds__(256) k_ecf_img_hist(const uint8_t* __restrict_
   auto add = [&](int c, int s) { asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(hs + 4u * c), "r"(s) : "memory"); };
   unsigned mx = 0;
   for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-    const int x = (int)(v % X);
-    const int64_t yz = v / X;
-    const int y = (int)(yz % Y), z = (int)(yz / Y);
+    int x, y, z;
+    if (HW < ((int64_t)1 << 31)) {  // 32-bit index math (the common case)
+      const int vi = (int)v, yz = vi / X;
+      x = vi - yz * X;
+      y = yz % Y;
+      z = yz / Y;
+    } else {
+      x = (int)(v % X);
+      const int64_t yz = v / X;
+      y = (int)(yz % Y);
+      z = (int)(yz / Y);
+    }
     ecf_anchor<ND>(px, v, x, y, z, X, Y, Z, add);
     const unsigned a = src[v];
     mx = a > mx ? a : mx;
