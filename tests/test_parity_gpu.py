@@ -488,3 +488,29 @@ def test_ecfx_full_size_vs_O2():
                         vweights=torch.from_numpy(cx.vweights).to(DEV)).cpu().numpy()
     w.sync_status()
     assert (out == oracle.ecf_complex(cx, f, 512)).all()
+
+
+def test_calls_are_cuda_graph_capturable():
+    """Every stream operation of a device-buffer call is capturable (stream-ordered
+    allocations, memsets, launches): capture wect_images / ecf_images once, replay, and
+    compare with the oracle (launch overhead of small calls goes away: cfg1 0.152 -> 0.130 ms
+    median per call on the B200)."""
+    c = synth.make_config(0)
+    img = torch.from_numpy(c["img"]).to(DEV)
+    dirs = torch.from_numpy(c["dirs"]).to(DEV)
+    out = torch.empty((1, 32, 64), dtype=torch.int32, device=DEV)
+    eout = torch.empty((1, 256), dtype=torch.int32, device=DEV)
+    w.wect_images(img, dirs, 64, out=out)
+    w.ecf_images(img, 256, lo=0.0, hi=255.0, out=eout)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        w.wect_images(img, dirs, 64, out=out)
+        w.ecf_images(img, 256, lo=0.0, hi=255.0, out=eout)
+    out.zero_()
+    eout.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == oracle.wect_images(c["img"], c["dirs"], 64)).all()
+    assert (eout.cpu().numpy() == oracle.ecf_images(c["img"], 256, 0.0, 255.0)).all()
