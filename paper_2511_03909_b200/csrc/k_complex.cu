@@ -366,7 +366,7 @@ wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float*
 wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                            const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
                            const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
-  if (mode == 1 || Dc <= kCellTile) {  // ECF, or few directions: one streaming pass, thread per cell
+  if (mode == 1 || Dc <= 3 * kCellTile) {  // ECF, or D <= 24: streaming passes (tiles of 8 filters), thread per cell
     const wect_status s = launch_stream(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp,
                                         wmax, diff, st, num_sms);
     if (s != WECT_ENOTSUP) return s;

@@ -514,3 +514,16 @@ def test_calls_are_cuda_graph_capturable():
     torch.cuda.synchronize()
     assert (out.cpu().numpy() == oracle.wect_images(c["img"], c["dirs"], 64)).all()
     assert (eout.cpu().numpy() == oracle.ecf_images(c["img"], 256, 0.0, 255.0)).all()
+
+
+@pytest.mark.parametrize("D", [9, 16, 17, 24])
+def test_streaming_path_multi_tile_directions_vs_O2(D):
+    """8 < D <= 24 runs the streaming kernel in tiles of 8 directions (grid.y): exact for
+    integer weights, A8 for float weights, on a mesh large enough to wrap the ring."""
+    g = np.random.default_rng(5000 + D)
+    cx = synth.torus_mesh(257, 311, D)
+    dirs = synth.directions_sphere(D, 3, 5100 + D)
+    assert (gpu_wect_complex(cx, dirs, 200) == oracle.wect_complex(cx, dirs, 200)).all()
+    cf = synth.random_small_complex(D, n=4, nverts=500, ntop=400, kmax=3, float_weights=True)
+    d4 = g.standard_normal((D, 4)).astype(np.float32)
+    assert_float_close(gpu_wect_complex(cf, d4, 77), oracle.wect_complex(cf, d4, 77), abs_cumsum(cf, d4, 77))
