@@ -317,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
         kname, bound = "k_grid_hist", "alu"
     elif wl["kind"] == "grad":
         kname, bound = "k_grad_cells", "alu"
-    elif wl["kind"] == "ecf" or D <= 8:
+    elif wl["kind"] == "ecf" or D <= 24:
         kname, bound = "k_stream", "hbm"
     else:
         kname, bound = "k_cells_vb", "alu"
