@@ -420,6 +420,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lane4 = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
+  constexpr int NPH = FREUD ? 8 : 4;  // phase (quadrant / chamber) slots
+  const bool phase_split = (int)gridDim.y >= NPH;
+  const int ysub = phase_split ? (int)blockIdx.y / NPH : (int)blockIdx.y;
+  const int nsub = phase_split ? (int)gridDim.y / NPH : (int)gridDim.y;
   if (threadIdx.x < 32) cwb[HW * 32 + threadIdx.x] = 0u;  // padding row: weight 0
 
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
@@ -448,7 +452,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
 #pragma unroll 1
     for (int o = 0; o < (FREUD ? 8 : 4); ++o) {
       const int qco = qcount[o];
-      if (qco == 0) continue;
+      // small batches: blockIdx.y splits the work over gridDim.y CTAs -- by phase when
+      // gridDim.y >= the phase count (then by direction within the phase), else by direction
+      if (phase_split && (int)blockIdx.y % NPH != o) continue;
+      if (ysub >= qco) continue;
       __syncthreads();  // pix staged / previous quadrant's sweeps done with cwb
       const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
       if (FREUD) {
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
         }
       }
       __syncthreads();
-      for (int k = warp; k < qco; k += kSweepWarps) {
+      for (int k = ysub + warp * nsub; k < qco; k += kSweepWarps * nsub) {
         const int dl = qlist[o * Dc + k];
         sweep_direction<OutT>(lane4, prog + (int64_t)dl * Lw, prog_len[dl], Lp, st, out, img0, nimg, Dc, dl, T, lane);
         __syncwarp();
@@ -771,7 +778,12 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   WECT_CUDA_TRY(cudaGetLastError());
   const size_t smem = sweep_smem_bytes(HW, T);
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
-  const int grid = (int)(ngroups < num_sms ? ngroups : num_sms);
+  // fewer image groups than SMs (small batches): split every phase's directions over CTAs
+  const int nph = freud ? 8 : 4;
+  int split = (int)(num_sms / (ngroups > 0 ? ngroups : 1));
+  split = split < 1 ? 1 : (split > kSweepWarps * nph ? kSweepWarps * nph : split);
+  if (split >= nph) split = (split / nph) * nph;  // whole phase rows: y = phase + nph * sub
+  const dim3 grid((unsigned)(ngroups < num_sms ? ngroups : num_sms), (unsigned)split);
   MainTimer timer(st);
 #define WECT_SWEEP(OT, FR)                                                                                   \
   do {                                                                                                       \
