@@ -563,24 +563,30 @@ def run_reference(args):
     wl = workload(args.config, 0)
     import oracle
 
-    per_step = 2000 if wl["kind"] == "images" else (400 if wl["kind"] == "ecfimg" and wl["B"] > 64 else
-                                                     (1 if wl["kind"] == "ecfimg" else None))
+    big_volume = wl["kind"] == "images" and wl["B"] == 1 and wl["img"][0].size > 1 << 20
+    if wl["kind"] == "images" and not big_volume:
+        per_step = min(50 if wl.get("freudenthal") else 2000, wl["B"])
+    elif wl["kind"] == "ecfimg":
+        per_step = min(400 if wl["B"] > 64 else 1, wl["B"])
+    else:
+        per_step = None  # one large complex: the bounded cpu_baseline sample, scaled
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        if wl["kind"] == "images":
-            oracle.wect_images(wl["img"][:per_step], wl["dirs"], wl["T"])
-            units = per_step
-        elif wl["kind"] == "ecfimg":
+        r = None
+        if per_step is not None and wl["kind"] == "images":
+            if wl.get("freudenthal"):
+                oracle.wect_images_freudenthal(wl["img"][:per_step], wl["dirs"], wl["T"])
+            else:
+                oracle.wect_images(wl["img"][:per_step], wl["dirs"], wl["T"])
+        elif per_step is not None:
             oracle.ecf_images(wl["img"][:per_step], wl["T"], 0.0, 255.0)
-            units = per_step
         else:
             r = cpu_baseline(wl)
-            units = None
         dt = time.perf_counter() - t0
         if i >= args.warmup:
-            times.append((dt, units, r if units is None else None))
-    if wl["kind"] in ("images", "ecfimg"):
+            times.append((dt, per_step, r))
+    if per_step is not None:
         tot = sum(t for t, _, _ in times)
         value = per_step * len(times) / tot
         sample = f"O2 on images [0, {per_step}) of the {wl['B']}-image workload per step"
