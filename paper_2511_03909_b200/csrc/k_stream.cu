@@ -18,6 +18,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "async.cuh"
 
 namespace wect {
 
@@ -37,27 +38,6 @@ struct StreamUnits {
 
 __host__ __device__ constexpr int stream_unit_cells(int ar) { return ar <= 4 ? kStreamUnit : kStreamUnit / 2; }
 
-// ---- mbarrier / bulk-copy PTX (sm_90+; CTA-local, no cluster)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  unsigned ok = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
 // L2 policy for the streamed index lists and weights: read once, so evict first -- the
 // gathered filter values / coordinates (re-read by every cell dimension) keep the L2.
 __device__ __forceinline__ uint64_t l2_evict_first() {

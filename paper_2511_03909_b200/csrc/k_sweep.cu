@@ -1,0 +1,618 @@
+// k_sweep.cu -- the image-batch WECT (wect_images on 2-D images of <= kSweepMaxHW pixels:
+// BASELINE configs[0] and configs[1]), cubical and Freudenthal.
+//
+// Geometry is image-independent, so per call k_sort2d reduces it, per direction, to a
+// RECORD PROGRAM: the vertices sorted by their exact binary64 bin (alpha, eq.
+// left-adjoint P:637-645, reading A1), grouped per bin into 16-byte records of up to 7
+// vertex rows.  Exact regrouping: for a direction s a
+// cubical cell's height is that of one designated corner (upper index on every axis with
+// s_k > 0), so all cells designating vertex v sum into one combined weight cw_o(v)
+// (o = quadrant of s, |cw| <= 255) and land in bin(v).
+//
+// k_sweep2d: a persistent CTA (16 warps, one per SM) takes 64 images at a time, stages
+// their pixels transposed, builds the quadrant's cw table in shared memory -- one 128-byte
+// row per vertex, word j = images (j, j+32) as a signed packed pair cw_j + cw_{j+32} 2^16 --
+// and each warp sweeps one direction: for every bin, its records' rows are gathered
+// (one LDS per row: every lane reads its own word of the same row) and summed, the sum is
+// unpacked onto two int32 running totals (images lane, lane+32).  The running total after
+// bin q IS the cumulative sum of the difference histogram (Alg. 1 lines 4-11):
+// no atomics, no separate scan, exact int32.  Bins are unrolled by output chunk (16 int32
+// / 8 int64 bins = 64 bytes per image), so every bin's total lands in a register; a chunk
+// goes to a per-warp 64-image x 64-byte shared stage (64B-swizzled: conflict-free
+// STS.128) and out to HBM with one TMA tensor store (cp.async.bulk.tensor), which takes
+// the strided [B, D, T] writes off the load/store pipe.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "async.cuh"
+
+namespace wect {
+
+constexpr int kRecRows = 15;     // vertex rows per 32-byte record (u16 header + 15 u16 rows)
+constexpr int kSweepWarps = 16;
+constexpr int kSweepImgs = 64;   // images per CTA group: lane l owns images l, l + 32
+constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
+constexpr int kStageRow = 32;    // bytes per image row of an output chunk (8 int32 / 4 int64 bins)
+constexpr int kStageBytes = kSweepImgs * kStageRow;  // per warp
+constexpr int kRingRecs = 32;    // per-warp record ring: two halves of 16 records (32 B each)
+constexpr int kRingBytes = kRingRecs * 32;
+constexpr int kSweepMaxHW = 1000;
+
+__host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
+// bins per output chunk for an output element of osz bytes (64-byte image rows)
+__host__ __device__ constexpr int chunk_bins(int osz) { return kStageRow / osz; }
+// 32-byte records per direction: one per bin at least, + one per 15 vertices, + the prefetch pad
+__host__ __device__ constexpr int sweep_rec_stride(int HW, int Tp) { return Tp + (HW + kRecRows - 1) / kRecRows + 8; }
+// smem of k_sweep2d: cw table [HW][128 B] (1024-aligned) | output stages [16][2 KB] |
+// record rings [16][1 KB] | ring mbarriers [16][2] | pixels [HW][68 B]
+__host__ __device__ constexpr size_t sweep_cw_bytes(int HW) { return align_up((size_t)HW * 128, 1024); }
+__host__ __device__ constexpr size_t sweep_fixed_bytes() {
+  return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16);
+}
+__host__ __device__ constexpr size_t sweep_smem_bytes(int HW) {
+  return 1024 + sweep_cw_bytes(HW) + sweep_fixed_bytes() + align_up((size_t)HW * kPixStride, 16);
+}
+
+// Freudenthal designated vertex (offset index: 0 self, 1 X = (r,c+1), 2 Y = (r+1,c),
+// 3 D = (r+1,c+1)) of simplex type t (1 e_x, 2 e_y, 3 e_diag, 4 U, 5 L) in chamber (A, B, C)
+// = (s_x > 0, s_y > 0, s_x + s_y > 0); its vertex set as a bit mask over {self, X, Y, D}.
+__host__ __device__ __forceinline__ int freud_des(int t, int A, int B, int C) {
+  switch (t) {
+    case 1: return A ? 1 : 0;
+    case 2: return B ? 2 : 0;
+    case 3: return C ? 3 : 0;
+    case 4: return (B && C) ? 3 : ((A && !B) ? 1 : 0);
+    case 5: return (A && C) ? 3 : ((B && !A) ? 2 : 0);
+  }
+  return 0;
+}
+__host__ __device__ __forceinline__ int freud_mask(int t) {
+  constexpr int m[6] = {0x1, 0x3, 0x5, 0x9, 0xB, 0xD};
+  return m[t];
+}
+
+// Binary-block record layout: a record's n rows occupy, for each set bit of n from the
+// top, a block of 8 / 4 / 2 / 1 slots at slots 0-7 / 8-11 / 12-13 / 14, so the sweep sums
+// them as up to four straight-line blocks of independent gathers (no per-row test).
+__host__ __device__ __forceinline__ int rec_slot(int n, int p) {
+  int base = 0;
+#pragma unroll
+  for (int blk = 8; blk >= 1; blk >>= 1) {
+    if (n & blk) {
+      if (p < blk) return base + p;
+      p -= blk;
+    }
+    base += blk;
+  }
+  return 14;
+}
+
+// ---------------------------------------------------------------------------
+// Per local direction (one CTA each): exact bins of all H*W vertices (binary64,
+// alpha64), counting sort by bin, and the direction's record program over Tp >= T bins:
+//   for bin q = 0 .. Tp-1, max(1, ceil(count_q / 15)) records of 32 bytes:
+//   u16 header (bits 0-3: rows n <= 15 in this record, bit 4: another record of the same
+//   bin follows), u16 slot[15] (vertex ids, any order within a bin, placed by rec_slot).
+// Bins q >= T are empty (the TMA store clips them).  Also records the direction's
+// quadrant / chamber in qlist, and (Freudenthal) the correction list.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __restrict__ dirs, int d_begin, int Dc,
+                                                const GridParams* __restrict__ gp, uint4* __restrict__ recs,
+                                                int rec_stride, int Tp, int* __restrict__ qlist,
+                                                int* __restrict__ qcount, int* __restrict__ nrecs, int freud,
+                                                int4* __restrict__ corr, int* __restrict__ ncorr, int corr_cap) {
+  // smem: counts[Tp], rbase[Tp], totals[Tp], vbin[HW] (u16)
+  extern __shared__ int sh[];
+  const GridParams g = *gp;
+  const int HW = H * W, dl = blockIdx.x, p = d_begin + dl;
+  int* counts = sh;
+  int* rbase = sh + Tp;
+  int* totals = sh + 2 * Tp;
+  uint16_t* vbin = (uint16_t*)(sh + 3 * Tp);
+  // rows in record j of a bin of c rows
+  auto counts_total_rows = [&](int q, int j) {
+    const int c = totals[q] - j * kRecRows;
+    return c < kRecRows ? c : kRecRows;
+  };
+  uint4* rec = recs + (int64_t)dl * rec_stride * 2;  // 32-byte records = 2 uint4
+  for (int q = threadIdx.x; q < Tp; q += blockDim.x) counts[q] = 0;
+  for (int k = threadIdx.x; k < 2 * rec_stride; k += blockDim.x) rec[k] = make_uint4(0, 0, 0, 0);
+  const float sx = dirs[2 * p], sy = dirs[2 * p + 1];
+  const int maxd = H > W ? H : W;
+  const double S = (double)(maxd - 1 > 1 ? maxd - 1 : 1);
+  __syncthreads();
+  for (int v = threadIdx.x; v < HW; v += blockDim.x) {
+    const int r = v / W, c = v % W;
+    const double h = __dadd_rn(__dmul_rn((double)axis_coord(c, W, S), (double)sx),
+                               __dmul_rn((double)axis_coord(r, H, S), (double)sy));
+    const int bq = alpha64(h, g);
+    vbin[v] = (uint16_t)bq;
+    atomicAdd(&counts[bq], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // record bases: exclusive scan of max(1, ceil(count / 7)) over bins
+    const int lane = threadIdx.x, per = (Tp + 31) / 32, q0 = lane * per;
+    int s = 0;
+    for (int q = q0; q < q0 + per && q < Tp; ++q) s += counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1;
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int base = incl - s;
+    for (int q = q0; q < q0 + per && q < Tp; ++q) {
+      rbase[q] = base;
+      base += counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1;
+    }
+    if (lane == 31) nrecs[dl] = incl;  // records of this direction's program
+    if (lane == 0) {
+      // cubical: quadrant (s_x > 0) | (s_y > 0) << 1; Freudenthal: chamber | (s_x + s_y > 0) << 2
+      const int o = (sx > 0.f ? 1 : 0) | (sy > 0.f ? 2 : 0) | ((freud && sx + sy > 0.f) ? 4 : 0);
+      const int slot = atomicAdd(&qcount[o], 1);
+      qlist[o * Dc + slot] = dl;
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < Tp; q += blockDim.x) {  // record headers
+    const int c = counts[q];
+    totals[q] = c;
+    const int nrec = c > kRecRows ? (c + kRecRows - 1) / kRecRows : 1;
+    for (int j = 0; j < nrec; ++j) {
+      const int n = c - j * kRecRows < kRecRows ? c - j * kRecRows : kRecRows;
+      ((uint16_t*)(rec + 2 * (rbase[q] + j)))[0] = (uint16_t)(n | (j + 1 < nrec ? 16 : 0));
+    }
+  }
+  if (freud) {
+    // Simplices whose chamber-designated vertex does not carry the simplex's max exact bin
+    // (only possible through the rounded diagonal comparison): the sweep counts them from
+    // bin lo = vbin[designated]; record [lo, hi) so k_sweep_fix moves them to hi.
+    const int A = sx > 0.f, B = sy > 0.f, C = (sx + sy) > 0.f;
+    for (int i = threadIdx.x; i < 5 * HW; i += blockDim.x) {
+      const int u = i / 5, t = 1 + (i - u * 5), r = u / W, c = u - r * W;
+      const bool rt = c + 1 < W, dn = r + 1 < H;
+      if ((t == 1 && !rt) || (t == 2 && !dn) || (t >= 3 && !(rt && dn))) continue;
+      const int off[4] = {0, 1, W, W + 1};
+      const int mask = freud_mask(t);
+      int hi = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (mask >> k & 1) hi = max(hi, (int)vbin[u + off[k]]);
+      const int lo = vbin[u + off[freud_des(t, A, B, C)]];
+      if (hi > lo) {
+        const int slot = atomicAdd(ncorr, 1);
+        if (slot < corr_cap) corr[slot] = make_int4(dl, u, t, lo | (hi << 16));
+      }
+    }
+  }
+  __syncthreads();  // headers written before the row slots of the same records
+  for (int v = threadIdx.x; v < HW; v += blockDim.x) {
+    const int bq = vbin[v];
+    const int r = atomicAdd(&counts[bq], -1) - 1;  // position within the bin
+    const int j = r / kRecRows, p = r - j * kRecRows;
+    const int n = counts_total_rows(bq, j);
+    ((uint16_t*)(rec + 2 * (rbase[bq] + j)))[1 + rec_slot(n, p)] = (uint16_t)v;
+  }
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m), "r"(src),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// stage byte offset of (image row r, 16-byte chunk j): 32-byte rows, CU_TENSOR_MAP_SWIZZLE_32B
+// (address bit 4 ^= bit 7); a quarter-warp writing rows r0..r0+7 hits 8 distinct 16-byte
+// bank groups.
+__device__ __forceinline__ uint32_t stage_off(int r, int j) { return (uint32_t)(r * kStageRow + 16 * (j ^ ((r >> 2) & 1))); }
+
+// Freudenthal combined weight of vertex (r, c) for chamber (A, B, C): the signed weights of
+// the simplices (anchored at v - delta) whose designated vertex is v (freud_des), packed
+// u16x2 for images (lane, lane+32): positives (vertex, U, L) minus negatives (3 edges),
+// each sum <= 765 per half.  p0 = this lane's pixel pair of vertex v in the staged rows.
+__device__ __forceinline__ uint32_t freud_cw(const uint8_t* p0, int r, int c, int H, int W, int A, int B, int C) {
+  auto P = [&](int dr, int dc) -> uint32_t {
+    return __byte_perm(*(const uint16_t*)(p0 + (dr * W + dc) * kPixStride), 0, 0x4140);
+  };
+  const bool up = r > 0, dn = r + 1 < H, lf = c > 0, rt = c + 1 < W;
+  const uint32_t a = P(0, 0);
+  uint32_t pos = a, neg = 0;
+  if (A) { if (lf) neg += __vmaxu2(a, P(0, -1)); } else if (rt) neg += __vmaxu2(a, P(0, 1));          // e_x
+  if (B) { if (up) neg += __vmaxu2(a, P(-1, 0)); } else if (dn) neg += __vmaxu2(a, P(1, 0));          // e_y
+  if (C) { if (up && lf) neg += __vmaxu2(a, P(-1, -1)); } else if (dn && rt) neg += __vmaxu2(a, P(1, 1));  // e_diag
+  if (B && C) { if (up && lf) pos += __vmaxu2(__vmaxu2(a, P(-1, -1)), P(-1, 0)); }                  // U
+  else if (A && !B) { if (lf && dn) pos += __vmaxu2(__vmaxu2(a, P(0, -1)), P(1, 0)); }
+  else if (rt && dn) pos += __vmaxu2(__vmaxu2(a, P(0, 1)), P(1, 1));
+  if (A && C) { if (up && lf) pos += __vmaxu2(__vmaxu2(a, P(-1, -1)), P(0, -1)); }                  // L
+  else if (B && !A) { if (up && rt) pos += __vmaxu2(__vmaxu2(a, P(-1, 0)), P(0, 1)); }
+  else if (dn && rt) pos += __vmaxu2(__vmaxu2(a, P(1, 0)), P(1, 1));
+  return pos - neg;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// shared address of cw row (u16 half of w) for this lane: base + row * 128 (LOP3/SHF + IMAD)
+__device__ __forceinline__ uint32_t row_lo(uint32_t base, uint32_t w) {
+  uint32_t r;
+  asm("{.reg .u32 t; and.b32 t, %1, 0xFFFF; shl.b32 t, t, 7; add.u32 %0, t, %2;}" : "=r"(r) : "r"(w), "r"(base));
+  return r;
+}
+__device__ __forceinline__ uint32_t row_hi(uint32_t base, uint32_t w) {
+  uint32_t r;
+  asm("{.reg .u32 t; shr.u32 t, %1, 16; shl.b32 t, t, 7; add.u32 %0, t, %2;}" : "=r"(r) : "r"(w), "r"(base));
+  return r;
+}
+
+// Per-warp record ring: the direction's program streams HBM/L2 -> shared memory through
+// two halves of 16 records (cp.async.bulk, one mbarrier per half), refilled 16 records
+// ahead of use, so the gathers never wait on an L2 round trip.
+struct Ring {
+  uint8_t* buf;   // kRingBytes
+  uint64_t* bar;  // [2]
+  uint32_t ph;    // bit h: parity of half h's next completion
+};
+__device__ __forceinline__ void ring_fill(const Ring& R, int h, const uint4* prog, int first, int nrec) {
+  const int n = nrec - first < 16 ? nrec - first : 16;
+  if (n <= 0) return;
+  mbar_arrive_expect_tx(R.bar + h, (unsigned)n * 32u);
+  bulk_g2s_plain(R.buf + h * (kRingBytes / 2), prog + 2 * first, (unsigned)n * 32u, R.bar + h);
+}
+
+// One warp, one direction, the CTA's 64 images: run the direction's record program.
+// lane_s = shared address of this lane's word of cw row 0 (row v at lane_s + 128 v); running
+// totals (B0, B1) of images (img0 + lane, img0 + lane + 32); chunk stage st (this warp's).
+template <typename OutT, bool TMA>
+__device__ __forceinline__ void sweep_direction(uint32_t lane_s, const uint4* __restrict__ prog, int nrec, Ring& R,
+                                                uint8_t* __restrict__ st, const CUtensorMap* tmap,
+                                                OutT* __restrict__ out, int64_t B, int64_t img0, int Dc, int dl,
+                                                int T, int Tp, int lane) {
+  constexpr int CB = chunk_bins((int)sizeof(OutT));
+  constexpr int PER = 16 / (int)sizeof(OutT);  // bins per 16-byte chunk
+  if (lane == 0) {
+    ring_fill(R, 0, prog, 0, nrec);
+    ring_fill(R, 1, prog, 16, nrec);
+  }
+  const uint32_t ring_s = smem_u32(R.buf);
+  int r = 0;  // records consumed
+  int B0 = 0, B1 = 0;
+  const uint32_t st_s = smem_u32(st);
+#pragma unroll 1
+  for (int q0 = 0; q0 < Tp; q0 += CB) {
+    int o0[CB], o1[CB];
+#pragma unroll
+    for (int k = 0; k < CB; ++k) {
+      uint32_t more;
+      do {
+        if ((r & 15) == 0) {  // entering a ring half
+          const int h = (r >> 4) & 1;
+          if (r >= 16) {  // the other half (records r-16 .. r-1) is consumed: refill it 16 ahead
+            __syncwarp();
+            if (lane == 0) ring_fill(R, h ^ 1, prog, r + 16, nrec);
+          }
+          mbar_wait(R.bar + h, (R.ph >> h) & 1u);
+          R.ph ^= 1u << h;
+        }
+        uint4 a, b;
+        const uint32_t ra = ring_s + (uint32_t)(r & (kRingRecs - 1)) * 32u;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(ra));
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(ra + 16));
+        ++r;
+        const uint32_t n = a.x & 15u;
+        more = a.x & 16u;
+        uint32_t S = 0;
+        if (n & 8u)
+          S = lds32(row_hi(lane_s, a.x)) + lds32(row_lo(lane_s, a.y)) + lds32(row_hi(lane_s, a.y)) +
+              lds32(row_lo(lane_s, a.z)) + lds32(row_hi(lane_s, a.z)) + lds32(row_lo(lane_s, a.w)) +
+              lds32(row_hi(lane_s, a.w)) + lds32(row_lo(lane_s, b.x));
+        if (n & 4u)
+          S += lds32(row_hi(lane_s, b.x)) + lds32(row_lo(lane_s, b.y)) + lds32(row_hi(lane_s, b.y)) +
+               lds32(row_lo(lane_s, b.z));
+        if (n & 2u) S += lds32(row_hi(lane_s, b.z)) + lds32(row_lo(lane_s, b.w));
+        if (n & 1u) S += lds32(row_hi(lane_s, b.w));
+        // signed packed pair S = s0 + s1 2^16 (mod 2^32), |s0|, |s1| <= 15 * 765
+        const int s0 = (int)(int16_t)(S & 0xFFFFu);
+        B0 += s0;
+        B1 += ((int)S - s0) >> 16;
+      } while (more);
+      o0[k] = B0;
+      o1[k] = B1;
+    }
+    // the previous chunk's TMA store has finished reading the stage
+    if (TMA && lane == 0) tma_wait_read_all();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < CB / PER; ++j) {
+      if (sizeof(OutT) == 4) {
+        *(int4*)(st + stage_off(lane, j)) = make_int4(o0[4 * j], o0[4 * j + 1], o0[4 * j + 2], o0[4 * j + 3]);
+        *(int4*)(st + stage_off(lane + 32, j)) = make_int4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
+      } else {
+        *(longlong2*)(st + stage_off(lane, j)) = make_longlong2(o0[2 * j], o0[2 * j + 1]);
+        *(longlong2*)(st + stage_off(lane + 32, j)) = make_longlong2(o1[2 * j], o1[2 * j + 1]);
+      }
+    }
+    if (TMA) {
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tma_store_3d(tmap, st_s, q0, dl, (int)img0);
+    } else {
+      __syncwarp();
+      // generic store (misaligned output / odd T): element by element with bounds
+      for (int e = lane; e < kSweepImgs * CB; e += 32) {
+        const int rr = e / CB, k = e - rr * CB;
+        const int64_t img = img0 + rr;
+        if (img < B && q0 + k < T) {
+          const OutT v = *(const OutT*)(st + stage_off(rr, k / PER) + (k % PER) * sizeof(OutT));
+          out[(img * Dc + dl) * (int64_t)T + q0 + k] = v;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();  // all lanes are done with the ring before the next direction refills it
+}
+
+template <typename OutT, bool FREUD, bool TMA>
+__global__ void __launch_bounds__(kSweepWarps * 32, 1)
+    k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint4* __restrict__ recs, int rec_stride,
+              const int* __restrict__ qlist, const int* __restrict__ qcount, const int* __restrict__ nrecs, int Dc,
+              int T, int Tp, OutT* __restrict__ out, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1024-aligned (the 64B-swizzle pattern of the TMA stores), kept in the shared window
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  const int HW = H * W;
+  uint32_t* cwb = (uint32_t*)smem;  // [HW][32] words: images (j, j+32) signed packed
+  uint8_t* stages = smem + sweep_cw_bytes(HW);
+  uint8_t* rings = stages + kSweepWarps * kStageBytes;
+  uint64_t* bars = (uint64_t*)(rings + kSweepWarps * kRingBytes);
+  uint8_t* pix = (uint8_t*)(bars + 2 * kSweepWarps);  // [HW][kPixStride] u8: byte 2j + h = image j + 32 h
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  uint8_t* st = stages + warp * kStageBytes;
+  Ring ring{rings + warp * kRingBytes, bars + 2 * warp, 0u};
+  if (threadIdx.x < 2 * kSweepWarps) mbar_init(bars + threadIdx.x, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const uint32_t lane_s = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
+  const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
+  constexpr int NPH = FREUD ? 8 : 4;  // phase (quadrant / chamber) slots
+  const bool phase_split = (int)gridDim.y >= NPH;
+  const int ysub = phase_split ? (int)blockIdx.y / NPH : (int)blockIdx.y;
+  const int nsub = phase_split ? (int)gridDim.y / NPH : (int)gridDim.y;
+
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t img0 = grp * kSweepImgs;
+    const int nimg = (int)((B - img0) < kSweepImgs ? (B - img0) : kSweepImgs);
+    __syncthreads();  // the previous group's sweeps are done with pix / cwb
+    // stage the group's pixels transposed: image i -> byte 2 (i % 32) + i / 32 of pix[v]
+    if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
+      const int per = HW >> 4;
+      for (int f = threadIdx.x; f < kSweepImgs * per; f += blockDim.x) {
+        const int i = f & (kSweepImgs - 1), v = (f >> 6) << 4;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (i < nimg) x = __ldcs((const uint4*)(img + (img0 + i) * HW + v));
+        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+        const int pos = 2 * (i & 31) + (i >> 5);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pix[(v + k) * kPixStride + pos] = (uint8_t)(wv[k >> 2] >> (8 * (k & 3)));
+      }
+    } else {
+      for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
+        const int i = f & (kSweepImgs - 1), v = f >> 6;
+        pix[v * kPixStride + 2 * (i & 31) + (i >> 5)] = i < nimg ? img[(img0 + i) * HW + v] : (uint8_t)0;
+      }
+    }
+#pragma unroll 1
+    for (int o = 0; o < NPH; ++o) {
+      const int qco = qcount[o];
+      // small batches: blockIdx.y splits the work over gridDim.y CTAs -- by phase when
+      // gridDim.y >= the phase count (then by direction within the phase), else by direction
+      if (phase_split && (int)blockIdx.y % NPH != o) continue;
+      if (ysub >= qco) continue;
+      __syncthreads();  // pix staged / previous phase's sweeps done with cwb
+      int v = threadIdx.x >> 5;
+      int r = v / W, c = v - r * W;
+      const int step_r = kSweepWarps / W, step_c = kSweepWarps - step_r * W;
+      if (FREUD) {
+        for (; v < HW; v += kSweepWarps) {
+          cwb[v * 32 + lane] = freud_cw(pix + v * kPixStride + 2 * lane, r, c, H, W, o & 1, (o >> 1) & 1, (o >> 2) & 1);
+          r += step_r;
+          c += step_c;
+          if (c >= W) { c -= W; ++r; }
+        }
+      } else {
+        // task (v, m): vertex v, staged pixel bytes 4m..4m+3 = images (2m, 2m+32, 2m+1, 2m+33)
+        // -> cw words 2m, 2m+1 as signed packed pairs cw_lo + cw_hi 2^16 (mod 2^32):
+        // (a + m_diag) - (m_c + m_r) per u16 half (each operand half <= 510, so a negative
+        // low half borrows into the high half exactly as the packed pair encodes it).
+        // Missing neighbours (grid border) drop their cells: m_c / m_r / m_diag = 0.
+        const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
+        const int m = threadIdx.x & 15;
+        const int v0 = threadIdx.x >> 4;  // 32 vertices per pass: step (32 / W, 32 % W) in (row, col)
+        int rr = v0 / W, cc = v0 - rr * W;
+        const int srow = (kSweepWarps * 2) / W, scol = (kSweepWarps * 2) - srow * W;
+        for (int vv = v0; vv < HW; vv += kSweepWarps * 2) {
+          const bool vc = (unsigned)(cc + dc) < (unsigned)W, vr = (unsigned)(rr + dr) < (unsigned)H;
+          const int oc = vc ? dc : 0, orr = vr ? dr * W : 0;
+          const uint8_t* p0 = pix + vv * kPixStride + 4 * m;
+          const uint32_t xa = *(const uint32_t*)p0;
+          const uint32_t xc = *(const uint32_t*)(p0 + oc * kPixStride);
+          const uint32_t xr = *(const uint32_t*)(p0 + orr * kPixStride);
+          const uint32_t xd = *(const uint32_t*)(p0 + (orr + oc) * kPixStride);
+          uint32_t cw[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t sel = h ? 0x4342u : 0x4140u;
+            const uint32_t A = __byte_perm(xa, 0, sel), C = __byte_perm(xc, 0, sel);
+            const uint32_t R = __byte_perm(xr, 0, sel), Dg = __byte_perm(xd, 0, sel);
+            const uint32_t MC = vc ? __vmaxu2(A, C) : 0u;
+            const uint32_t MR = vr ? __vmaxu2(A, R) : 0u;
+            const uint32_t MD = (vc && vr) ? __vmaxu2(__vmaxu2(MC, MR), Dg) : 0u;
+            cw[h] = (A + MD) - (MC + MR);
+          }
+          *(uint2*)(cwb + vv * 32 + 2 * m) = make_uint2(cw[0], cw[1]);
+          rr += srow;
+          cc += scol;
+          if (cc >= W) { cc -= W; ++rr; }
+        }
+      }
+      __syncthreads();
+      for (int k = ysub + warp * nsub; k < qco; k += kSweepWarps * nsub) {
+        const int dl = __shfl_sync(0xffffffffu, qlist[o * Dc + k], 0);
+        sweep_direction<OutT, TMA>(lane_s, recs + (int64_t)dl * rec_stride * 2, nrecs[dl], ring, st, &tmap, out, B,
+                                   img0, Dc, dl, T, Tp, lane);
+      }
+    }
+  }
+  if (TMA && lane == 0) tma_wait_all();
+}
+
+// Freudenthal corrections (after k_sweep2d): simplex (dl, u, t) was counted from bin lo but
+// belongs to bin hi > lo: subtract its signed weight from the cumulative bins [lo, hi).
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_sweep_fix(const uint8_t* __restrict__ img, int64_t B, int H, int W,
+                                                   const int4* __restrict__ corr, const int* __restrict__ ncorr,
+                                                   int Dc, int T, OutT* __restrict__ out) {
+  const int64_t n = (int64_t)*ncorr * B;
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / B, b = i - e * B;
+    const int4 c = corr[e];
+    const uint8_t* p = img + b * HW + c.y;
+    const int off[4] = {0, 1, W, W + 1};
+    const int mask = freud_mask(c.z);
+    int mx = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (mask >> k & 1) mx = max(mx, (int)p[off[k]]);
+    const int sw = (c.z >= 4) ? mx : -mx;  // (-1)^dim: edges -1, triangles +1
+    if (sw == 0) continue;
+    OutT* row = out + (b * Dc + c.x) * (int64_t)T;
+    for (int q = c.w & 0xFFFF; q < (c.w >> 16); ++q) {
+      if (sizeof(OutT) == 4) atomicAdd((int*)(row + q), -sw);
+      else atomicAdd((unsigned long long*)(row + q), (unsigned long long)(long long)(-sw));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+// TMA map of out [B][Dc][T] (element osz bytes), box [64 images][1][CB bins], 32B swizzle.
+// false: not expressible (alignment / strides) -> the generic store path.
+static bool make_out_map(CUtensorMap* m, void* out, int64_t B, int Dc, int T, int osz) {
+  if (((uintptr_t)out & 15) != 0 || ((int64_t)T * osz) % 16 != 0 || B > 0xFFFFFFFFll) return false;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)T, (cuuint64_t)Dc, (cuuint64_t)B};
+  const cuuint64_t strides[2] = {(cuuint64_t)T * osz, (cuuint64_t)Dc * T * osz};
+  const cuuint32_t box[3] = {(cuuint32_t)chunk_bins(osz), 1u, (cuuint32_t)kSweepImgs};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  const CUresult r = enc(m, osz == 4 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_INT64, 3, out, dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
+  if (ndim != 2) return false;
+  const int64_t HW = dims[0] * dims[1];
+  return HW >= 1 && HW <= kSweepMaxHW && T <= 4096 && sweep_smem_bytes((int)HW) <= 227 * 1024;
+}
+
+static int padded_bins(int T) { return (T + 7) & ~7; }  // a whole number of chunks for int32 and int64
+
+size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud) {
+  return (size_t)Dc * sweep_rec_stride(HW, padded_bins(T)) * 32 + 64 + (size_t)(8 + 9 * Dc + 1) * 4 + 64 +
+         (freud ? (size_t)5 * HW * Dc * sizeof(int4) + 16 : 0);
+}
+
+wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc,
+                           int T, const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
+                           int num_sms, int freud) {
+  const int HW = H * W;
+  const int Tp = padded_bins(T);
+  const int rstride = sweep_rec_stride(HW, Tp);
+  uint4* recs = (uint4*)align_up((uintptr_t)scratch, 16);
+  int* ints = (int*)align_up((uintptr_t)(recs + (size_t)Dc * rstride * 2), 16);
+  int* qcount = ints;           // 8 chamber slots (cubical uses 4)
+  int* qlist = ints + 8;        // [8][Dc]
+  int* nrecs = qlist + 8 * Dc;  // [Dc]
+  int* ncorr = nrecs + Dc;
+  int4* corr = (int4*)align_up((uintptr_t)(ncorr + 1), 16);
+  const int corr_cap = freud ? 5 * HW * Dc : 0;
+  WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 8 * sizeof(int), st));
+  WECT_CUDA_TRY(cudaMemsetAsync(ncorr, 0, sizeof(int), st));
+  const size_t sort_smem = (size_t)3 * Tp * sizeof(int) + align_up((size_t)HW * 2, 16);
+  if (sort_smem > 48 * 1024)
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sort2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
+  k_sort2d<<<Dc, 256, sort_smem, st>>>(H, W, dirs, d_begin, Dc, gp, recs, rstride, Tp, qlist, qcount, nrecs, freud,
+                                       corr, ncorr, corr_cap);
+  count_launch();
+  WECT_CUDA_TRY(cudaGetLastError());
+  const size_t smem = sweep_smem_bytes(HW);
+  const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
+  // fewer image groups than SMs (small batches): split every phase's directions over CTAs
+  const int nph = freud ? 8 : 4;
+  int split = (int)(num_sms / (ngroups > 0 ? ngroups : 1));
+  split = split < 1 ? 1 : (split > kSweepWarps * nph ? kSweepWarps * nph : split);
+  if (split >= nph) split = (split / nph) * nph;  // whole phase rows: y = phase + nph * sub
+  const dim3 grid((unsigned)(ngroups < num_sms ? ngroups : num_sms), (unsigned)split);
+  const int osz = odtype == WECT_I32 ? 4 : 8;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  const bool tma = getenv("WECT_SWEEP_NOTMA") == nullptr && make_out_map(&tmap, out, B, Dc, T, osz);
+  MainTimer timer(st);
+#define WECT_SWEEP(OT, FR, TM)                                                                                      \
+  do {                                                                                                              \
+    WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<OT, FR, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_sweep2d<OT, FR, TM><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, recs, rstride, qlist, qcount, nrecs, Dc, T, \
+                                                                 Tp, (OT*)out, tmap);                                   \
+    count_launch();                                                                                                 \
+  } while (0)
+#define WECT_SWEEP_T(OT, FR) \
+  do {                       \
+    if (tma) WECT_SWEEP(OT, FR, true); else WECT_SWEEP(OT, FR, false); \
+  } while (0)
+  if (odtype == WECT_I32) {
+    if (freud) WECT_SWEEP_T(int32_t, true); else WECT_SWEEP_T(int32_t, false);
+  } else {
+    if (freud) WECT_SWEEP_T(long long, true); else WECT_SWEEP_T(long long, false);
+  }
+#undef WECT_SWEEP_T
+#undef WECT_SWEEP
+  timer.stop();
+  if (freud) {  // the rare rounded-diagonal simplices (usually none)
+    const int fb = num_sms * 4;
+    if (odtype == WECT_I32) k_sweep_fix<int32_t><<<fb, 256, 0, st>>>(img, B, H, W, corr, ncorr, Dc, T, (int32_t*)out);
+    else k_sweep_fix<long long><<<fb, 256, 0, st>>>(img, B, H, W, corr, ncorr, Dc, T, (long long*)out);
+    count_launch();
+  }
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+}  // namespace wect
