@@ -39,7 +39,7 @@ constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: confli
 constexpr int kStageRow = 32;    // bytes per image row of an output chunk (8 int32 / 4 int64 bins)
 constexpr int kStageBytes = kSweepImgs * kStageRow;  // per warp
 constexpr int kRingRecs = 32;    // per-warp record ring: two halves of 16 records (32 B each)
-constexpr int kRingBytes = kRingRecs * 32;
+constexpr int kRingBytes = kRingRecs * 32;  // 1 KB: halves at byte 0 and 512 (ro >> 9)
 constexpr int kSweepMaxHW = 1000;
 
 __host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
@@ -284,7 +284,8 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane_s, const uint4* __
     ring_fill(R, 1, prog, 16, nrec);
   }
   const uint32_t ring_s = smem_u32(R.buf);
-  int r = 0;  // records consumed
+  uint32_t ro = 0;   // byte offset of the next record in the ring (32 records of 32 B)
+  int fill = 32;     // first record of the next refill
   int B0 = 0, B1 = 0;
   const uint32_t st_s = smem_u32(st);
 #pragma unroll 1
@@ -294,20 +295,20 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane_s, const uint4* __
     for (int k = 0; k < CB; ++k) {
       uint32_t more;
       do {
-        if ((r & 15) == 0) {  // entering a ring half
-          const int h = (r >> 4) & 1;
-          if (r >= 16) {  // the other half (records r-16 .. r-1) is consumed: refill it 16 ahead
-            __syncwarp();
-            if (lane == 0) ring_fill(R, h ^ 1, prog, r + 16, nrec);
-          }
+        if ((ro & (kRingBytes / 2 - 1)) == 0) {  // entering a ring half
+          const int h = (int)(ro >> 9);
           mbar_wait(R.bar + h, (R.ph >> h) & 1u);
           R.ph ^= 1u << h;
         }
         uint4 a, b;
-        const uint32_t ra = ring_s + (uint32_t)(r & (kRingRecs - 1)) * 32u;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(ra));
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(ra + 16));
-        ++r;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(ring_s + ro));
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(ring_s + ro + 16));
+        ro = (ro + 32u) & (kRingBytes - 1);
+        if ((ro & (kRingBytes / 2 - 1)) == 0 && fill < nrec) {  // left a half: refill it 32 records ahead
+          __syncwarp();
+          if (lane == 0) ring_fill(R, (int)(ro >> 9) ^ 1, prog, fill, nrec);
+          fill += 16;
+        }
         const uint32_t n = a.x & 15u;
         more = a.x & 16u;
         uint32_t S = 0;
@@ -431,39 +432,40 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
           if (c >= W) { c -= W; ++r; }
         }
       } else {
-        // task (v, m): vertex v, staged pixel bytes 4m..4m+3 = images (2m, 2m+32, 2m+1, 2m+33)
-        // -> cw words 2m, 2m+1 as signed packed pairs cw_lo + cw_hi 2^16 (mod 2^32):
-        // (a + m_diag) - (m_c + m_r) per u16 half (each operand half <= 510, so a negative
-        // low half borrows into the high half exactly as the packed pair encodes it).
-        // Missing neighbours (grid border) drop their cells: m_c / m_r / m_diag = 0.
+        // task (row rr, m): pixel bytes 4m..4m+3 of the row's vertices = images (2m, 2m+32, 2m+1,
+        // 2m+33) -> cw words 2m, 2m+1 of every vertex of the row, as signed packed pairs
+        // cw_lo + cw_hi 2^16 (mod 2^32): (a + m_diag) - (m_c + m_r) per u16 half (each operand half
+        // <= 510, so a negative low half borrows into the high half exactly as the packed pair
+        // encodes it).  The row is walked against dc, so the column neighbour (c + dc) and its
+        // row neighbour are the previous step's pixels (2 loads per vertex).  Missing
+        // neighbours (grid border) drop their cells: m_c / m_r / m_diag = 0.
         const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
-        const int m = threadIdx.x & 15;
-        const int v0 = threadIdx.x >> 4;  // 32 vertices per pass: step (32 / W, 32 % W) in (row, col)
-        int rr = v0 / W, cc = v0 - rr * W;
-        const int srow = (kSweepWarps * 2) / W, scol = (kSweepWarps * 2) - srow * W;
-        for (int vv = v0; vv < HW; vv += kSweepWarps * 2) {
-          const bool vc = (unsigned)(cc + dc) < (unsigned)W, vr = (unsigned)(rr + dr) < (unsigned)H;
-          const int oc = vc ? dc : 0, orr = vr ? dr * W : 0;
-          const uint8_t* p0 = pix + vv * kPixStride + 4 * m;
-          const uint32_t xa = *(const uint32_t*)p0;
-          const uint32_t xc = *(const uint32_t*)(p0 + oc * kPixStride);
-          const uint32_t xr = *(const uint32_t*)(p0 + orr * kPixStride);
-          const uint32_t xd = *(const uint32_t*)(p0 + (orr + oc) * kPixStride);
-          uint32_t cw[2];
+        for (int t = threadIdx.x; t < H * 16; t += kSweepWarps * 32) {
+          const int rr = t >> 4, m = t & 15;
+          const bool vr = (unsigned)(rr + dr) < (unsigned)H;
+          const int orr = vr ? dr * W * kPixStride : 0;
+          const int c0 = dc > 0 ? W - 1 : 0;
+          const uint8_t* p0 = pix + (rr * W + c0) * kPixStride + 4 * m;
+          uint32_t* q0 = cwb + (rr * W + c0) * 32 + 2 * m;
+          uint32_t Cp[2] = {0u, 0u}, Dp[2] = {0u, 0u};
+          for (int step = 0; step < W; ++step) {
+            const uint32_t xa = *(const uint32_t*)p0, xr = *(const uint32_t*)(p0 + orr);
+            uint32_t cw[2];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t sel = h ? 0x4342u : 0x4140u;
-            const uint32_t A = __byte_perm(xa, 0, sel), C = __byte_perm(xc, 0, sel);
-            const uint32_t R = __byte_perm(xr, 0, sel), Dg = __byte_perm(xd, 0, sel);
-            const uint32_t MC = vc ? __vmaxu2(A, C) : 0u;
-            const uint32_t MR = vr ? __vmaxu2(A, R) : 0u;
-            const uint32_t MD = (vc && vr) ? __vmaxu2(__vmaxu2(MC, MR), Dg) : 0u;
-            cw[h] = (A + MD) - (MC + MR);
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t sel = h ? 0x4342u : 0x4140u;
+              const uint32_t A = __byte_perm(xa, 0, sel), R = __byte_perm(xr, 0, sel);
+              const uint32_t MC = step > 0 ? __vmaxu2(A, Cp[h]) : 0u;
+              const uint32_t MR = vr ? __vmaxu2(A, R) : 0u;
+              const uint32_t MD = (step > 0 && vr) ? __vmaxu2(__vmaxu2(MC, MR), Dp[h]) : 0u;
+              cw[h] = (A + MD) - (MC + MR);
+              Cp[h] = A;
+              Dp[h] = R;
+            }
+            *(uint2*)q0 = make_uint2(cw[0], cw[1]);
+            p0 -= dc * kPixStride;
+            q0 -= dc * 32;
           }
-          *(uint2*)(cwb + vv * 32 + 2 * m) = make_uint2(cw[0], cw[1]);
-          rr += srow;
-          cc += scol;
-          if (cc >= W) { cc -= W; ++rr; }
         }
       }
       __syncthreads();
