@@ -23,8 +23,10 @@
  * Conventions shared by all calls
  *   - Pointers: every array pointer may be CUDA device memory or host memory
  *     (pageable or pinned); the library detects which.  Host inputs are staged
- *     to the device and host outputs are copied back inside the call, which then
- *     synchronises the stream.  Device-only calls are asynchronous on `stream`.
+ *     to the device and host outputs are copied back inside the call; a call
+ *     with any host array synchronises the stream before returning, so host
+ *     buffers may be reused at once.  Device-only calls are asynchronous on
+ *     `stream` (device inputs must stay untouched until the stream completes).
  *   - Ownership: the caller owns every array.  The library keeps no pointer
  *     after the call's stream work completes; it allocates its scratch with
  *     cudaMallocAsync on `stream` and frees it stream-ordered.
@@ -37,7 +39,10 @@
  *     unspecified).  With WECT_VALIDATE the indices are checked synchronously
  *     first and WECT_ERANGE is returned with nothing written.
  *   - wect_last_error() returns a thread-local message for the last failure.
- *   - Reentrant; distinct calls may run concurrently on distinct streams.
+ *   - Reentrant; distinct calls may run concurrently on distinct streams.  The
+ *     deferred-error word (WECT_ERANGE) and the repair counter are PER DEVICE,
+ *     not per call: with concurrent calls on one device, wect_sync_status() on
+ *     one stream can report an out-of-range index found by another call.
  */
 #ifndef WECT_H_
 #define WECT_H_

@@ -89,10 +89,26 @@ def _grid(T, d_begin, d_count, maxheight, lo, hi, flags):
 
 
 def _alloc_out(shape, torch_dtype_name, dev, out):
+    """A fresh output tensor, or the caller's out= after checking that the library may
+    write exactly prod(shape) elements of torch_dtype_name into it (the C ABI only sees a
+    pointer: a short, mistyped or strided out would be written out of bounds)."""
     torch = _torch()
-    if out is not None:
-        return out
     td = getattr(torch, torch_dtype_name)
+    if out is not None:
+        if not _is_torch(out):
+            raise TypeError("out must be a torch tensor")
+        n = 1
+        for d in shape:
+            n *= int(d)
+        if out.numel() != n:
+            raise ValueError(f"out has {out.numel()} elements, expected {n} (shape {tuple(shape)})")
+        if out.dtype != td:
+            raise ValueError(f"out dtype {out.dtype} does not match the output dtype {td}")
+        if dev is not None and out.device != dev:
+            raise ValueError(f"out is on {out.device}, inputs on {dev}")
+        if not out.is_contiguous():
+            raise ValueError("out must be contiguous")
+        return out
     return torch.empty(shape, dtype=td, device=dev if dev is not None else "cpu")
 
 

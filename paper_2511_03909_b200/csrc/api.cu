@@ -135,6 +135,7 @@ struct Arena {
   cudaStream_t st;
   std::vector<void*> blocks;
   cudaError_t err = cudaSuccess;
+  bool staged = false;  // some input was host memory: the call syncs before returning
   explicit Arena(cudaStream_t s) : st(s) {}
   ~Arena() {
     for (void* b : blocks) cudaFreeAsync(b, st);
@@ -153,6 +154,7 @@ struct Arena {
     if (!d) return nullptr;
     cudaError_t e = cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { err = e; return nullptr; }
+    staged = true;
     return d;
   }
 };
@@ -189,11 +191,12 @@ static OutView out_view(Arena& ar, void* user, size_t bytes) {
   if (user && !is_device_ptr(user)) o.dev = ar.alloc(bytes);
   return o;
 }
-static wect_status out_finish(const OutView& o, cudaStream_t st) {
-  if (o.dev != o.user) {
-    WECT_CUDA_TRY(cudaMemcpyAsync(o.user, o.dev, o.bytes, cudaMemcpyDeviceToHost, st));
-    WECT_CUDA_TRY(cudaStreamSynchronize(st));
-  }
+// Host outputs are copied back; if any input or output was host memory the stream is
+// synchronised, so the caller may reuse (or read) its host buffers when the call returns
+// (a pinned input would otherwise still be read by an in-flight DMA).
+static wect_status out_finish(const OutView& o, Arena& ar) {
+  if (o.dev != o.user) WECT_CUDA_TRY(cudaMemcpyAsync(o.user, o.dev, o.bytes, cudaMemcpyDeviceToHost, ar.st));
+  if (o.dev != o.user || ar.staged) WECT_CUDA_TRY(cudaStreamSynchronize(ar.st));
   return WECT_OK;
 }
 
@@ -335,6 +338,7 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
     const int64_t per_img = nv * (1 << ndim) * 2;
     int64_t chunk = ((int64_t)1 << 30) / per_img;
     if (chunk < 1) chunk = 1;
+    if (chunk > 65535) chunk = 65535;  // k_grid_hist takes the image from gridDim.z
     if (chunk > B) chunk = B;
     int16_t* cwo = (int16_t*)ar.alloc((size_t)chunk * per_img);
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
@@ -346,7 +350,7 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
   }
   if (s != WECT_OK) return s;
-  return out_finish(ov, st);
+  return out_finish(ov, ar);
 }
 
 // -------------------------------------------------------------- image ECF
@@ -389,7 +393,7 @@ wect_status ecf_images(const uint8_t* img, int64_t B, int32_t ndim, const int64_
   if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging", __FILE__, __LINE__);
   wect_status s = launch_ecf_images(dimg, B, ndim, dims, grid->T, mode, lo, hi, scr, ov.dev, odtype, st, nsm);
   if (s != WECT_OK) return s;
-  return out_finish(ov, st);
+  return out_finish(ov, ar);
 }
 
 // ----------------------------------------------------- explicit complexes
@@ -445,7 +449,7 @@ static wect_status run_complex(int mode, const wect_complex_desc* K, const float
   if (ar.err != cudaSuccess) return fail_cuda(ar.err, "staging", __FILE__, __LINE__);
   if (K->k0 == 0) {  // empty complex: every WECF is 0
     WECT_CUDA_TRY(cudaMemsetAsync(ov.dev, 0, obytes, st));
-    return out_finish(ov, st);
+    return out_finish(ov, ar);
   }
   const size_t wsz = 4;
   Segs segs;
@@ -517,7 +521,7 @@ static wect_status run_complex(int mode, const wect_complex_desc* K, const float
   if (s != WECT_OK) return s;
   s = launch_finalize(diff, floatw, Dc, T, ov.dev, odtype, st);
   if (s != WECT_OK) return s;
-  return out_finish(ov, st);
+  return out_finish(ov, ar);
 }
 
 // ------------------------------------------------ backward (weights gradient)
@@ -581,7 +585,7 @@ static wect_status run_complex_grad(int mode, const wect_complex_desc* K, const 
   if (K->k0 == 0) return WECT_OK;
   if (Dc == 0) {  // no rows: the gradient is 0
     for (auto& v : views) WECT_CUDA_TRY(cudaMemsetAsync(v.dev, 0, v.bytes, st));
-    for (auto& v : views) { s = out_finish(v, st); if (s != WECT_OK) return s; }
+    for (auto& v : views) { s = out_finish(v, ar); if (s != WECT_OK) return s; }
     return WECT_OK;
   }
   const float* coords = mode == 0 ? (const float*)ar.in(K->coords, (size_t)K->k0 * n * 4) : nullptr;
@@ -608,7 +612,7 @@ static wect_status run_complex_grad(int mode, const wect_complex_desc* K, const 
   s = launch_complex_grad(mode, n, segs, coords, K->k0, dsrc, D, d_begin, Dc, T, gp, dG, gout, st, nsm);
   if (s != WECT_OK) return s;
   for (auto& v : views) {
-    s = out_finish(v, st);
+    s = out_finish(v, ar);
     if (s != WECT_OK) return s;
   }
   return WECT_OK;

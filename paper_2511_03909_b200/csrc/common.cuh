@@ -160,4 +160,30 @@ struct MainTimer {
 };
 wect_status fail_cuda(cudaError_t e, const char* what, const char* file, int line);
 wect_status fail(wect_status s, const char* fmt, ...);
+
+// Stream-ordered scratch: every block allocated through it is freed (cudaFreeAsync on the
+// same stream) when the owner goes out of scope -- also on the early error returns of
+// WECT_CUDA_TRY, so no path leaks pool memory.
+struct AsyncScratch {
+  cudaStream_t st;
+  void* p[8] = {};
+  int n = 0;
+  explicit AsyncScratch(cudaStream_t s) : st(s) {}
+  AsyncScratch(const AsyncScratch&) = delete;
+  AsyncScratch& operator=(const AsyncScratch&) = delete;
+  ~AsyncScratch() {
+    for (int i = 0; i < n; ++i) cudaFreeAsync(p[i], st);
+  }
+  template <typename Tp>
+  cudaError_t alloc(Tp** out, size_t bytes) {
+    *out = nullptr;
+    if (n == 8) return cudaErrorMemoryAllocation;
+    void* q = nullptr;
+    const cudaError_t e = cudaMallocAsync(&q, bytes ? bytes : 16, st);
+    if (e != cudaSuccess) return e;
+    p[n++] = q;
+    *out = (Tp*)q;
+    return cudaSuccess;
+  }
+};
 }  // namespace wect

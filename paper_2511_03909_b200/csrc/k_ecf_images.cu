@@ -547,10 +547,18 @@ static wect_status launch_ecf_images_t(const uint8_t* img, int64_t B, int ndim, 
   unsigned long long* ghist = (unsigned long long*)((char*)scratch + off);
   unsigned int* gmax = (unsigned int*)(ghist + (size_t)B * 256);
   WECT_CUDA_TRY(cudaMemsetAsync(ghist, 0, (size_t)B * 256 * 8 + (size_t)B * 4, st));
+  // the rows kernel stages kEcfRows + 1 image rows: only when they fit the opt-in shared memory
+  const size_t rows_smem = 2048 + (size_t)kEcfWarps * 2048 + (size_t)(kEcfRows + 1) * ((X + 2) >> 1) * 4;
+  int smem_optin = 0;
+  {
+    int dev = 0;
+    WECT_CUDA_TRY(cudaGetDevice(&dev));
+    WECT_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  }
   const bool rows_path = ndim == 2 && X % 4 == 0 && X <= 16384 && ((uintptr_t)img & 3) == 0 &&
-                         !getenv("WECT_ECF_GENERIC");
+                         rows_smem <= (size_t)smem_optin && !getenv("WECT_ECF_GENERIC");
   if (rows_path) {
-    const size_t smem = 2048 + (size_t)kEcfWarps * 2048 + (size_t)(kEcfRows + 1) * ((X + 2) >> 1) * 4;
+    const size_t smem = rows_smem;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_ecf_img2d_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 g((unsigned)((Y + kEcfRows - 1) / kEcfRows), (unsigned)B);
     MainTimer timer(st);

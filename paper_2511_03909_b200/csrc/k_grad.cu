@@ -184,10 +184,11 @@ wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* 
                                 const GradOut& gout, cudaStream_t st, int num_sms) {
   for (int i = 0; i < segs.nseg; ++i)
     if (segs.s[i].arity > 8) return fail(WECT_ENOTSUP, "backward supports cells of arity <= 8");
+  AsyncScratch mem(st);  // freed on every return path
   double* RC = nullptr;
   uint32_t* vb = nullptr;
-  WECT_CUDA_TRY(cudaMallocAsync((void**)&RC, (size_t)Dc * T * sizeof(double), st));
-  WECT_CUDA_TRY(cudaMallocAsync((void**)&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t), st));
+  WECT_CUDA_TRY(mem.alloc(&RC, (size_t)Dc * T * sizeof(double)));
+  WECT_CUDA_TRY(mem.alloc(&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t)));
   k_rcumsum<<<(unsigned)((Dc + 127) / 128), 128, 0, st>>>(G, Dc, T, RC); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
   const size_t smem = (size_t)T * 32 * sizeof(double);
@@ -242,8 +243,6 @@ wect_status launch_complex_grad(int mode, int n, const Segs& segs, const float* 
       if (e != cudaSuccess) s = fail_cuda(e, "k_grad_cells", __FILE__, __LINE__);
     }
   }
-  cudaFreeAsync(RC, st);
-  cudaFreeAsync(vb, st);
   return s;
 }
 

@@ -442,8 +442,9 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
   Segs segs = segs_in;
   for (int i = 0; i < segs.nseg; ++i)
     if (segs.s[i].arity > 7) return WECT_ENOTSUP;  // records hold <= 7 ids: k_complex takes it
+  AsyncScratch mem(st);  // freed on every return path
   uint32_t* vb = nullptr;
-  WECT_CUDA_TRY(cudaMallocAsync((void**)&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t), st));
+  WECT_CUDA_TRY(mem.alloc(&vb, (size_t)(k0 > 0 ? k0 : 1) * 32 * sizeof(uint32_t)));
   const size_t smem = (size_t)T * 64 * 4 + (size_t)kVbWarps * kVbBatch * 8 * sizeof(int);
   const int ctas = num_sms;  // one 1024-thread CTA per SM
   const int ntiles = (Dc + kVbTile - 1) / kVbTile;
@@ -470,7 +471,7 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
   }
   int64_t* bnd = nullptr;
   void* scratch = nullptr;
-  WECT_CUDA_TRY(cudaMallocAsync((void**)&bnd, sizeof(int64_t) * kMaxSegs * (nstep + 1), st));
+  WECT_CUDA_TRY(mem.alloc(&bnd, sizeof(int64_t) * kMaxSegs * (nstep + 1)));
   if (!bucket) {
     k_uniform_bnd<<<segs.nseg, 256, 0, st>>>(segs, nstep, bnd);
     count_launch();
@@ -480,7 +481,7 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
     for (int i = 0; i < segs.nseg; ++i)
       if (segs.s[i].verts) bytes += (size_t)segs.s[i].count * (segs.s[i].arity + 1) * 4 + 256;
     size_t cbytes = sizeof(int) * kBucketMax + 2 * sizeof(int64_t) * (kBucketMax + 1);
-    WECT_CUDA_TRY(cudaMallocAsync(&scratch, bytes + cbytes, st));
+    WECT_CUDA_TRY(mem.alloc(&scratch, bytes + cbytes));
     int* cnt = (int*)scratch;
     int64_t* cur = (int64_t*)((char*)scratch + sizeof(int) * kBucketMax);
     char* dst = (char*)scratch + cbytes;
@@ -512,8 +513,8 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
   }
   int* bat = nullptr;
   int64_t* bound = nullptr;
-  WECT_CUDA_TRY(cudaMallocAsync((void**)&bat, sizeof(int) * kMaxSegs * nstep, st));
-  WECT_CUDA_TRY(cudaMallocAsync((void**)&bound, sizeof(int64_t) * nstep, st));
+  WECT_CUDA_TRY(mem.alloc(&bat, sizeof(int) * kMaxSegs * nstep));
+  WECT_CUDA_TRY(mem.alloc(&bound, sizeof(int64_t) * nstep));
   k_step_info<<<(nstep + 255) / 256, 256, 0, st>>>(segs, nstep, bnd, ctas * kVbWarps, kVbWarps, bat, bound);
   count_launch();
   int vblocks = (int)((k0 + 255) / 256);
@@ -536,11 +537,6 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) s = fail_cuda(e, "k_cells_vb", __FILE__, __LINE__);
   }
-  cudaFreeAsync(vb, st);
-  cudaFreeAsync(bnd, st);
-  cudaFreeAsync(bat, st);
-  cudaFreeAsync(bound, st);
-  if (scratch) cudaFreeAsync(scratch, st);
   return s;
 }
 

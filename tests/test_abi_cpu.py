@@ -108,3 +108,27 @@ def test_new_entry_points_reject_bad_arguments_synchronously():
     gf = _lib.wect_grid(8, 0, 0, 0.0, 0.0, 0.0, _lib.FREUDENTHAL)
     assert L.wect_images(vol.ctypes.data, 1, 3, d3, dirs.ctypes.data, 2, ctypes.byref(gf), o3.ctypes.data, _lib.I32,
                          None) == _lib.ENOTSUP
+
+
+def test_out_argument_is_validated_before_the_call():
+    """a caller-supplied out= with the wrong size, dtype or layout is rejected in
+    the binding (the C ABI only sees a pointer and would write out of bounds)."""
+    import numpy as np
+    import torch
+
+    import paper_2511_03909_b200 as w
+
+    img = np.zeros((2, 4, 4), np.uint8)
+    dirs = np.zeros((3, 2), np.float32)
+    with pytest.raises(ValueError, match="elements"):
+        w.wect_images(img, dirs, 8, out=torch.empty((2, 3, 7), dtype=torch.int32))
+    with pytest.raises(ValueError, match="dtype"):
+        w.wect_images(img, dirs, 8, out=torch.empty((2, 3, 8), dtype=torch.int64))
+    with pytest.raises(ValueError, match="contiguous"):
+        w.wect_images(img, dirs, 8, out=torch.empty((2, 8, 3), dtype=torch.int32).transpose(1, 2))
+    with pytest.raises(ValueError, match="elements"):
+        w.ecf_images(img, 16, out=torch.empty((2, 15), dtype=torch.int32))
+    coords = np.zeros((3, 2), np.float32)
+    cells = [(np.array([[0, 1]], np.int32), np.array([1], np.int32), 1)]
+    with pytest.raises(ValueError, match="dtype"):
+        w.wect_complex(coords, cells, dirs, 8, out=torch.empty((3, 8), dtype=torch.int32))

@@ -183,6 +183,14 @@ def test_grid_coords_hand(golden):
     assert oracle.grid_coords(e["dims"]).tolist() == e["expected"]
 
 
+def test_grid_coords_hand_3d(golden):
+    """A volume's axis mapping (slice -> axis 2, row -> axis 1, column -> axis 0) against
+    hand values: an axis swap or a wrong S fails."""
+    e = golden["hand_values"]["grid_coords_2x3x4"]
+    got = oracle.grid_coords(e["dims"])[e["vertices"]]
+    assert np.array_equal(got, np.array(e["expected"], np.float64).astype(np.float32))
+
+
 def test_cubical_counts(golden):
     for case in golden["hand_values"]["cubical_counts"]["cases"]:
         img = np.zeros(case["dims"], np.uint8)
