@@ -11,10 +11,14 @@ cumsum, 1.97 GB output write).
 
   python bench.py [--gpus N --steps K --warmup W] [--config 1|2|3|4|ecfx|ecfimg|ecfimg1k|bwd3|bwd4|freud] [--impl reference]
 
-Multi-GPU (torchrun, one rank per GPU): images are sharded by batch with no data-path
-collective (weak scaling: every rank runs its own 60,000-image shard); times are the
-max over ranks (all_reduce MAX).  --impl reference times the CPU oracle (O2) on the
-host on a bounded sample of the same workload.
+Multi-GPU (one rank per GPU; `--gpus N` relaunches itself under torch.distributed.run when
+WORLD_SIZE is unset): STRONG scaling over the workload BASELINE.json names -- the one
+60,000-image batch is split into contiguous image shards (no data-path collective), a
+single volume / mesh is split into direction rows with M all-reduced (MAX) from per-shard
+maxima (reading A2), the weights gradient all-reduces (SUM) its partials.  Times are the
+max over ranks (all_reduce MAX); the all_gather that would assemble the full output is
+timed separately (`gather_ms`).  --impl reference times the CPU oracle (O2) on the host on
+a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -134,7 +138,7 @@ def workload(cfg: str, rank: int):
         c = int(cfg)
         spec = dict(synth.CONFIGS[c])
         B, dims = spec["B"], spec["dims"]
-        seed = synth.S0 + c + 7919 * rank
+        seed = synth.S0 + c  # one batch for every rank: ranks take shards of it (strong scaling)
         img = synth.images_u8(B, dims, seed, "uniform" if c != 2 else "uniform")
         n = len(dims)
         dirs = synth.directions_s1(spec["D"]) if n == 2 else synth.directions_sphere(spec["D"], n, synth.S0 + 30)
@@ -151,7 +155,7 @@ def workload(cfg: str, rank: int):
         # one bin per intensity): FMNIST-shaped 60k x 28x28, or 'padded ImageNet' 1000^2
         B, dims, kind, seed = (60000, (28, 28), "fmnist", synth.S0 + 60) if cfg == "ecfimg" else \
             (64, (1000, 1000), "uniform", synth.S0 + 61)
-        img = synth.images_u8(B, dims, seed + 7919 * rank, kind)
+        img = synth.images_u8(B, dims, seed, kind)
         nv = int(np.prod(dims))
         ncells = int(np.prod([2 * d - 1 for d in dims]))
         T = 256
@@ -196,10 +200,40 @@ def workload(cfg: str, rank: int):
 
 
 # ------------------------------------------------------------- our arm (GPU)
+def plan_shard(wl, world, rank):
+    """How rank `rank` of `world` shares the workload:
+    batch      -- image batches: contiguous image shards, no collective in the data path;
+    directions -- one volume / mesh / gradient: contiguous direction rows, M from an
+                  all_reduce(MAX) of per-shard maxima (reading A2), gradients all_reduce(SUM);
+    replicas   -- one tiny image or one filter (nothing to split): every rank the same call."""
+    from paper_2511_03909_b200.dist import shard_range
+
+    if world == 1:
+        return dict(mode="single", lo=0, hi=None, scaling="weak", parallelism="single GPU")
+    if wl["kind"] in ("images", "ecfimg") and wl["B"] > 1:
+        lo, hi = shard_range(wl["B"], world, rank)
+        return dict(mode="batch", lo=lo, hi=hi, scaling="strong", parallelism=f"image-batch shards x{world}")
+    if wl["kind"] in ("images", "complex", "grad"):
+        lo, hi = shard_range(wl["dirs"].shape[0], world, rank)
+        return dict(mode="directions", lo=lo, hi=hi, scaling="strong", parallelism=f"direction-row shards x{world}")
+    return dict(mode="replicas", lo=0, hi=None, scaling="weak", parallelism=f"replicas x{world}")
+
+
+def _allreduce(vals, op, dev):
+    import torch
+    import torch.distributed as dist
+
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=op)
+    return [float(x) for x in t.cpu()]
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
     import paper_2511_03909_b200 as w
+    from paper_2511_03909_b200 import dist as wdist
 
     dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
@@ -211,22 +245,42 @@ def run_ours(args, rank, world, local_rank):
         wl["alg_bytes"] += (args.D - synth.CONFIGS[int(args.config)]["D"]) * wl["T"] * 8
         wl["name"] += f"_D{args.D}"
     stream = torch.cuda.current_stream(dev)
+    sh = plan_shard(wl, world, rank)
+    # this rank's share of the work (units, updates, bytes) for the roofline of its kernels
+    if sh["mode"] == "batch":
+        frac = (sh["hi"] - sh["lo"]) / wl["B"]
+    elif sh["mode"] == "directions":
+        frac = (sh["hi"] - sh["lo"]) / wl["dirs"].shape[0]
+    else:
+        frac = 1.0
+    rows = None if sh["mode"] != "directions" else (sh["lo"], sh["hi"] - sh["lo"])
+    gather = None  # (local output, total rows, dim) for the separately timed all_gather
 
     if wl["kind"] == "ecfimg":
-        img_d = torch.from_numpy(wl["img"]).to(dev)
-        out_d = torch.empty((wl["B"], wl["T"]), dtype=torch.int32, device=dev)
+        lo, hi = (sh["lo"], sh["hi"]) if sh["mode"] == "batch" else (0, wl["B"])
+        img_d = torch.from_numpy(wl["img"][lo:hi]).to(dev)
+        out_d = torch.empty((hi - lo, wl["T"]), dtype=torch.int32, device=dev)
+        gather = (out_d, wl["B"], 0) if sh["mode"] == "batch" else None
 
         def step(flags=0):
             w.ecf_images(img_d, wl["T"], lo=0.0, hi=255.0, out=out_d, flags=flags)
     elif wl["kind"] == "images":
-        img_d = torch.from_numpy(wl["img"]).to(dev)
+        lo, hi = (sh["lo"], sh["hi"]) if sh["mode"] == "batch" else (0, wl["B"])
+        img_d = torch.from_numpy(wl["img"][lo:hi]).to(dev)
         dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
-        out_d = torch.empty((wl["B"], wl["dirs"].shape[0], wl["T"]),
-                            dtype=getattr(torch, wl["out_dtype"]), device=dev)
+        nrows = rows[1] if rows else wl["dirs"].shape[0]
+        out_d = torch.empty((hi - lo, nrows, wl["T"]), dtype=getattr(torch, wl["out_dtype"]), device=dev)
+        if sh["mode"] == "batch":
+            gather = (out_d, wl["B"], 0)
+        elif sh["mode"] == "directions":
+            gather = (out_d, wl["dirs"].shape[0], 1)
+        d0, dc = rows if rows else (0, 0)
 
         def step(flags=0):
-            w.wect_images(img_d, dirs_d, wl["T"], out_dtype=wl["out_dtype"], out=out_d, flags=flags,
-                          freudenthal=wl.get("freudenthal", False))
+            # direction shards pass the FULL direction set + their rows: the grid M is the
+            # analytic max over the bounding-box corners and ALL directions (reading A2)
+            w.wect_images(img_d, dirs_d, wl["T"], d_begin=d0, d_count=dc, out_dtype=wl["out_dtype"], out=out_d,
+                          flags=flags, freudenthal=wl.get("freudenthal", False))
     else:
         cx = wl["cx"]
         cells = [(torch.from_numpy(c.verts).to(dev), None if c.weights is None else torch.from_numpy(c.weights).to(dev),
@@ -237,9 +291,14 @@ def run_ours(args, rank, world, local_rank):
             dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
             G_d = torch.from_numpy(wl["G"]).to(dev)
             out_d = G_d
+            grad_group = None
 
             def step(flags=0):
-                w.wect_complex_backward(coords_d, cells, dirs_d, wl["T"], G_d, flags=flags)
+                if sh["mode"] == "directions":
+                    # partial gradients of this rank's rows, all_reduce(SUM) (the path's one exchange)
+                    wdist.wect_complex_backward_sharded(coords_d, cells, dirs_d, wl["T"], G_d, flags=flags)
+                else:
+                    w.wect_complex_backward(coords_d, cells, dirs_d, wl["T"], G_d, flags=flags)
         elif wl["kind"] == "ecf":
             f_d = torch.from_numpy(wl["fvals"]).to(dev)
             out_d = torch.empty((1, wl["T"]), dtype=torch.float64 if cx.is_float else torch.int64, device=dev)
@@ -249,12 +308,21 @@ def run_ours(args, rank, world, local_rank):
         else:
             coords_d = torch.from_numpy(cx.coords).to(dev)
             dirs_d = torch.from_numpy(wl["dirs"]).to(dev)
-            out_d = torch.empty((wl["dirs"].shape[0], wl["T"]), dtype=torch.float64 if cx.is_float else torch.int64,
-                                device=dev)
+            nrows = rows[1] if rows else wl["dirs"].shape[0]
+            out_d = torch.empty((nrows, wl["T"]), dtype=torch.float64 if cx.is_float else torch.int64, device=dev)
+            if sh["mode"] == "directions":
+                gather = (out_d, wl["dirs"].shape[0], 0)
+            d0, dc = rows if rows else (0, 0)
 
             def step(flags=0):
-                w.wect_complex(coords_d, cells, dirs_d, wl["T"], vweights=vw, is_float=cx.is_float, out=out_d,
-                               flags=flags)
+                if sh["mode"] == "directions":
+                    # M over ALL directions from per-shard maxima (reading A2): max is exact
+                    M = wdist.global_maxheight(coords_d, dirs_d)
+                    w.wect_complex(coords_d, cells, dirs_d, wl["T"], vweights=vw, is_float=cx.is_float, d_begin=d0,
+                                   d_count=dc, maxheight=M, out=out_d, flags=flags)
+                else:
+                    w.wect_complex(coords_d, cells, dirs_d, wl["T"], vweights=vw, is_float=cx.is_float, out=out_d,
+                                   flags=flags)
 
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
@@ -300,12 +368,26 @@ def run_ours(args, rank, world, local_rank):
 
     main_ms = tms / max(tl, 1)
     if world > 1:
-        t = torch.tensor([total_ms, main_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms, main_ms = float(t[0]), float(t[1])
+        total_ms, main_ms = _allreduce([total_ms, main_ms], torch.distributed.ReduceOp.MAX, dev)
+    # the all_gather that would assemble the full output on every rank (NCCL), timed apart
+    gather_ms = None
+    if world > 1 and gather is not None:
+        local, n_total, gdim = gather
+        wdist.gather_rows(local, n_total, gdim)  # warm-up (communicator buffers)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = wdist.gather_rows(local, n_total, gdim)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = _allreduce([g0.elapsed_time(g1)], torch.distributed.ReduceOp.MAX, dev)[0]
+        del full
 
     ms_per_step = total_ms / K
-    value = world * wl["units"] * K / (total_ms / 1e3)
+    # strong scaling: the shards add up to ONE workload; replicas: every rank does a whole one
+    mult = 1 if sh["scaling"] == "strong" else world
+    value = mult * wl["units"] * K / (total_ms / 1e3)
     peak, peak_src = load_peaks()
     per_call_launches = tl / max(K, 1)  # timed (dominant-kernel) launches per step
     D = wl["dirs"].shape[0] if "dirs" in wl else 1
@@ -322,14 +404,14 @@ def run_ours(args, rank, world, local_rank):
     else:
         kname, bound = "k_cells_vb", "alu"
     if bound == "hbm":
-        achieved = wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9
+        achieved = frac * wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9
         roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
-                "alg_bytes_per_launch": wl["alg_bytes"] / per_call_launches}
+                "alg_bytes_per_launch": frac * wl["alg_bytes"] / per_call_launches}
     else:
         # algorithmic work = shared-memory histogram updates: (cell, direction) pairs for
         # explicit complexes, regrouped (vertex, direction) pairs for voxel grids
-        work = wl["atomics"] / per_call_launches
+        work = frac * wl["atomics"] / per_call_launches
         apeak = alu_peak(float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0))
                          if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0)
         achieved = work / (main_ms / 1e3) / 1e9
@@ -337,7 +419,7 @@ def run_ours(args, rank, world, local_rank):
                 "frac": achieved * 1e9 / apeak,
                 "peak_source": "148 SMs x 16 shared int32 atomic lane-ops/clk (tools/microbench/smem_ubench.cu) x sm_max_mhz",
                 "work_per_launch": work,
-                "hbm_achieved_gbs": wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9}
+                "hbm_achieved_gbs": frac * wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9}
     traffic = load_traffic(f"cfg{args.config}" + (f"_D{args.D}" if args.D else ""))
     res = {
         "metric": METRIC,
@@ -348,105 +430,91 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": sh["scaling"],
         "vs_baseline": None,
         "dtype": "int32" if wl.get("out_dtype") == "int32" else ("f64" if wl["kind"] == "grad" or ("cx" in wl and wl["cx"].is_float) else "int64"),
         "data": "synthetic (seeded; DESIGN.md input recipe)",
-        "config": {"workload": wl["name"], "desc": wl["desc"], "per_gpu_units": wl["units"],
+        "config": {"workload": wl["name"], "desc": wl["desc"],
+                   "per_gpu_units": wl["units"] * frac if sh["scaling"] == "strong" else wl["units"],
+                   "shard": {"mode": sh["mode"], "lo": sh["lo"], "hi": sh["hi"]},
                    "l2": f"flushed between timed steps ({flush.numel() >> 20} MiB write, untimed)",
-                   "parallelism": f"batch-sharded dp{world}" if wl["kind"] in ("images", "ecfimg") else f"replicas x{world}"},
+                   "parallelism": sh["parallelism"]},
+        "gather_ms": gather_ms,
         "step_ms_p50": float(np.percentile(step_ms, 50)),
         "step_ms_p99": float(np.percentile(step_ms, 99)),
         "warm_l2_ms_per_step": warm_ms,
-        "updates_per_s": world * wl["updates"] * K / (total_ms / 1e3),
-        "hbm_gbs": world * wl["alg_bytes"] * K / (total_ms / 1e3) / 1e9,
+        "updates_per_s": mult * wl["updates"] * K / (total_ms / 1e3),
+        "hbm_gbs": mult * wl["alg_bytes"] * K / (total_ms / 1e3) / 1e9,
         "roofline": dict(roof, traffic=traffic, kernel_ms=main_ms, launches_per_step=per_call_launches,
                          kernel_share_of_step=main_ms * per_call_launches / ms_per_step),
         "gpu_launches": int(launches),
         "repairs_binary64": int(repairs),
         "clocks": sampler.summary(),
     }
-    # end to end through the public API with HOST buffers (H2D + compute + D2H every step)
-    if not args.no_e2e and wl["kind"] == "ecfimg":
-        img_h = torch.from_numpy(wl["img"]).pin_memory()
-        out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
-        for _ in range(2):
-            w.ecf_images(img_h, wl["T"], lo=0.0, hi=255.0, out=out_h)
-        ke = max(1, min(5, K))
-        if world > 1:
-            torch.distributed.barrier()
-        t0 = time.perf_counter()
-        for _ in range(ke):
-            w.ecf_images(img_h, wl["T"], lo=0.0, hi=255.0, out=out_h)
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t[0])
-        res["e2e"] = {"value": world * wl["units"] * ke / e2e_s, "unit": wl["unit"],
-                      "h2d_bytes_per_step": int(img_h.numel()),
-                      "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()), "steps": ke,
-                      "path": "ecf_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"}
-    elif not args.no_e2e and wl["kind"] == "images":
-        img_h = torch.from_numpy(wl["img"]).pin_memory()
-        dirs_h = torch.from_numpy(wl["dirs"])
-        out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
-        fr = wl.get("freudenthal", False)
-        for _ in range(2):
-            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h, freudenthal=fr)
-        ke = max(1, min(5, K))
-        if world > 1:
-            torch.distributed.barrier()
-        t0 = time.perf_counter()
-        for _ in range(ke):
-            w.wect_images(img_h, dirs_h, wl["T"], out_dtype=wl["out_dtype"], out=out_h, freudenthal=fr)
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t[0])
-        res["e2e"] = {"value": world * wl["units"] * ke / e2e_s, "unit": wl["unit"],
-                      "h2d_bytes_per_step": int(img_h.numel() + dirs_h.numel() * 4),
-                      "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()), "steps": ke,
-                      "path": "wect_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"}
-    elif not args.no_e2e and wl["kind"] == "grad":
-        cx = wl["cx"]
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        cells_h = [(pin(c.verts), None, c.dim) for c in cx.cells]
-        coords_h, dirs_h, G_h = pin(cx.coords), pin(wl["dirs"]), pin(wl["G"])
-        gv, gc = w.wect_complex_backward(coords_h, cells_h, dirs_h, wl["T"], G_h)  # warm-up (pool, modules)
-        t0 = time.perf_counter()
-        ke = 2
-        for _ in range(ke):
-            gv, gc = w.wect_complex_backward(coords_h, cells_h, dirs_h, wl["T"], G_h)
-        e2e_s = time.perf_counter() - t0
-        res["e2e"] = {"value": world * ke / e2e_s, "unit": wl["unit"],
-                      "h2d_bytes_per_step": int(cx.coords.nbytes + sum(c.verts.nbytes for c in cx.cells) + wl["G"].nbytes),
-                      "d2h_bytes_per_step": int(8 * (gv.numel() + sum(g.numel() for g in gc))), "steps": ke}
-    elif not args.no_e2e:
-        cx = wl["cx"]
+    # end to end through the public API with HOST buffers (H2D + compute + D2H every step),
+    # each rank on its own shard, max over ranks
+    if not args.no_e2e:
         pin = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        cells_h = [(pin(c.verts), pin(c.weights), c.dim) for c in cx.cells]
-        vw_h, coords_h = pin(cx.vweights), pin(cx.coords)
-        src_h = pin(wl["fvals"]) if wl["kind"] == "ecf" else pin(wl["dirs"])
-        out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
+        d0, dc = rows if rows else (0, 0)
+        if wl["kind"] in ("ecfimg", "images"):
+            lo, hi = (sh["lo"], sh["hi"]) if sh["mode"] == "batch" else (0, wl["B"])
+            img_h = pin(wl["img"][lo:hi])
+            out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
+            if wl["kind"] == "ecfimg":
+                h2d = img_h.numel()
+                path = "ecf_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"
 
-        def e2e_step():
-            if wl["kind"] == "ecf":
-                return w.ecf_complex(src_h, cells_h, wl["T"], vweights=vw_h, is_float=cx.is_float, out=out_h)
-            return w.wect_complex(coords_h, cells_h, src_h, wl["T"], vweights=vw_h, is_float=cx.is_float, out=out_h)
+                def e2e_step():
+                    return w.ecf_images(img_h, wl["T"], lo=0.0, hi=255.0, out=out_h)
+            else:
+                dirs_h = torch.from_numpy(wl["dirs"])
+                h2d = img_h.numel() + dirs_h.numel() * 4
+                path = "wect_images(host pinned in, host pinned out): library stages H2D, D2H, syncs"
 
-        o = e2e_step()  # warm-up
+                def e2e_step():
+                    return w.wect_images(img_h, dirs_h, wl["T"], d_begin=d0, d_count=dc, out_dtype=wl["out_dtype"],
+                                         out=out_h, freudenthal=wl.get("freudenthal", False))
+            ke = max(1, min(5, K))
+        elif wl["kind"] == "grad":
+            cx = wl["cx"]
+            cells_h = [(pin(c.verts), None, c.dim) for c in cx.cells]
+            coords_h, dirs_h, G_h = pin(cx.coords), pin(wl["dirs"]), pin(wl["G"][d0:d0 + dc] if rows else wl["G"])
+            h2d = cx.coords.nbytes + sum(c.verts.nbytes for c in cx.cells) + G_h.numel() * 8
+            path = "wect_complex_backward(host pinned in, host out) per rank's rows"
+
+            def e2e_step():
+                gv, gc = w.wect_complex_backward(coords_h, cells_h, dirs_h, wl["T"], G_h, d_begin=d0, d_count=dc)
+                return torch.cat([gv] + list(gc))
+            ke = 2
+        else:
+            cx = wl["cx"]
+            cells_h = [(pin(c.verts), pin(c.weights), c.dim) for c in cx.cells]
+            vw_h, coords_h = pin(cx.vweights), pin(cx.coords)
+            src_h = pin(wl["fvals"]) if wl["kind"] == "ecf" else pin(wl["dirs"])
+            out_h = torch.empty(tuple(out_d.shape), dtype=out_d.dtype).pin_memory()
+            h2d = (cx.coords.nbytes if wl["kind"] != "ecf" else wl["fvals"].nbytes) + sum(
+                c.verts.nbytes + (c.weights.nbytes if c.weights is not None else 0) for c in cx.cells) + (
+                cx.vweights.nbytes if cx.vweights is not None else 0)
+            path = "wect_complex / ecf_complex(host pinned in, host pinned out) per rank's rows"
+
+            def e2e_step():
+                if wl["kind"] == "ecf":
+                    return w.ecf_complex(src_h, cells_h, wl["T"], vweights=vw_h, is_float=cx.is_float, out=out_h)
+                M = wdist.global_maxheight(coords_h, src_h) if rows else 0.0
+                return w.wect_complex(coords_h, cells_h, src_h, wl["T"], vweights=vw_h, is_float=cx.is_float,
+                                      d_begin=d0, d_count=dc, maxheight=M, out=out_h)
+            ke = 2
+        o = e2e_step()  # warm-up (pool, modules)
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        ke = 2
         for _ in range(ke):
             o = e2e_step()
         e2e_s = time.perf_counter() - t0
-        h2d = (cx.coords.nbytes if wl["kind"] != "ecf" else wl["fvals"].nbytes) + sum(
-            c.verts.nbytes + (c.weights.nbytes if c.weights is not None else 0) for c in cx.cells) + (
-            cx.vweights.nbytes if cx.vweights is not None else 0)
-        res["e2e"] = {"value": world * ke / e2e_s, "unit": wl["unit"], "h2d_bytes_per_step": int(h2d),
-                      "d2h_bytes_per_step": int(o.numel() * o.element_size()), "steps": ke}
+        if world > 1:
+            e2e_s = _allreduce([e2e_s], torch.distributed.ReduceOp.MAX, dev)[0]
+        res["e2e"] = {"value": mult * wl["units"] * ke / e2e_s, "unit": wl["unit"], "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(o.numel() * o.element_size()), "steps": ke, "path": path}
     # the CPU oracle beside it (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
@@ -603,6 +671,20 @@ def run_reference(args):
             "e2e": {"value": value, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def relaunch(n):
+    """`bench.py --gpus N` without a launcher: run N ranks under torch.distributed.run on this
+    node (127.0.0.1); rank 0 prints the JSON line.  Returns the launcher's exit code."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -624,12 +706,21 @@ def main():
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     if world > 1:
         import torch
 
         dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
         torch.cuda.set_device(dev)
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        if torch.cuda.device_count() >= world:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init log (NVLS / P2P / rings) to stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:  # more ranks than GPUs (a logic check on a small box): gloo for the host-side collectives
+            print(f"bench: {world} ranks on {torch.cuda.device_count()} GPU(s): gloo, ranks share devices",
+                  file=sys.stderr)
+            torch.distributed.init_process_group("gloo")
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)

@@ -88,6 +88,32 @@ def wect_images_sharded(img: torch.Tensor, dirs: torch.Tensor, T: int, *, mode: 
     raise ValueError(mode)
 
 
+def _lib_maxheight(coords, dirs):
+    from . import wect_maxheight
+
+    return wect_maxheight(coords, dirs)
+
+
+def global_maxheight(coords, dirs, *, group=None, compute: Optional[Callable] = None) -> float:
+    """M = max over ALL directions and vertices of |<x_v, s_p>| (reading A2) from
+    per-shard maxima: rank r evaluates only its direction rows shard_range(D, world, r)
+    (wect_maxheight on that contiguous slice) and all_reduce(MAX) combines them.  Exact: each
+    shard's M is the exact binary64 maximum and max is associative.  Direction-sharded
+    calls pass it as `maxheight`, so no rank scans the full direction set."""
+    compute = compute or _lib_maxheight
+    world, rank = _world(group)
+    D = int(dirs.shape[0])
+    lo, hi = shard_range(D, world, rank)
+    m = float(compute(coords, dirs[lo:hi])) if hi > lo else 0.0
+    if world > 1:
+        on_dev = dist.get_backend(group) == "nccl"
+        t = torch.tensor([m], dtype=torch.float64,
+                         device=torch.device("cuda", torch.cuda.current_device()) if on_dev else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        m = float(t.item())
+    return m
+
+
 def _lib_complex(coords, cells, dirs, T, d_begin, d_count, **kw):
     from . import wect_complex
 
@@ -95,12 +121,16 @@ def _lib_complex(coords, cells, dirs, T, d_begin, d_count, **kw):
 
 
 def wect_complex_sharded(coords, cells: Sequence[Tuple], dirs, T: int, *, gather: bool = True, group=None,
-                         compute: Optional[Callable] = None, **kw) -> torch.Tensor:
+                         compute: Optional[Callable] = None, maxheight_compute: Optional[Callable] = None,
+                         **kw) -> torch.Tensor:
     """WECT of one explicit complex, direction-sharded: rank r computes the rows
-    shard_range(D, world, r) with M over ALL directions (reading A2), then all_gather."""
+    shard_range(D, world, r) with M over ALL directions (reading A2) -- all-reduced from the
+    per-shard maxima (global_maxheight) unless the caller fixes `maxheight` -- then all_gather."""
     compute = compute or _lib_complex
     world, rank = _world(group)
     D = int(dirs.shape[0])
+    if kw.get("maxheight", 0.0) <= 0.0 and world > 1:
+        kw["maxheight"] = global_maxheight(coords, dirs, group=group, compute=maxheight_compute)
     lo, hi = shard_range(D, world, rank)
     if hi > lo:
         local = compute(coords, cells, dirs, T, lo, hi - lo, **kw)

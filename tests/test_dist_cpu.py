@@ -13,8 +13,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2511_03909_b200.dist import (ecf_images_sharded, gather_rows, shard_range, wect_complex_backward_sharded,
-                                        wect_complex_sharded, wect_images_sharded)
+from paper_2511_03909_b200.dist import (ecf_images_sharded, gather_rows, global_maxheight, shard_range,
+                                        wect_complex_backward_sharded, wect_complex_sharded, wect_images_sharded)
 
 
 def test_shard_range_partitions():
@@ -38,8 +38,12 @@ def _oracle_images(img, dirs, T, d_begin, d_count, **kw):
 
 def _oracle_complex(coords, cells, dirs, T, d_begin, d_count, **kw):
     cx = synth.Complex(coords, kw["vweights"], [synth.Cells(v, w, d) for v, w, d in cells], coords.shape[0])
-    full = oracle.wect_complex(cx, dirs, T)
+    full = oracle.wect_complex(cx, dirs, T, maxheight_override=kw.get("maxheight", 0.0))
     return torch.from_numpy(full[d_begin:d_begin + d_count].copy())
+
+
+def _oracle_maxheight(coords, dirs):
+    return oracle.maxheight(oracle.heights(coords, np.asarray(dirs)))
 
 
 def _oracle_ecf_images(img, T, **kw):
@@ -81,7 +85,10 @@ def _worker(rank, world, port, q):
         d3 = synth.directions_sphere(5, 3, 1)
         d3[4] *= 3.0  # the row that sets M lives on the last rank
         cref = oracle.wect_complex(cx, d3, 12)
-        c = wect_complex_sharded(cx.coords, cells, d3, 12, compute=_oracle_complex, vweights=cx.vweights)
+        c = wect_complex_sharded(cx.coords, cells, d3, 12, compute=_oracle_complex,
+                                 maxheight_compute=_oracle_maxheight, vweights=cx.vweights)
+        # M from per-shard maxima (all_reduce MAX) equals M over all directions, exactly
+        mh = global_maxheight(cx.coords, d3, compute=_oracle_maxheight) == _oracle_maxheight(cx.coords, d3)
         # image ECF (NEXT-1): batch shards, no exchange
         eimg = torch.from_numpy(g.integers(0, 256, (5, 6, 8), dtype=np.uint8))
         eref = oracle.ecf_images(eimg.numpy(), 32, 0.0, 255.0)
@@ -92,7 +99,7 @@ def _worker(rank, world, port, q):
         gv, gc = wect_complex_backward_sharded(cx.coords, cells, d3, 12, G, compute=_oracle_backward)
         gok = np.array_equal(gv.numpy(), gv_ref) and all(np.array_equal(a_.numpy(), b_) for a_, b_ in zip(gc, gc_ref))
         q.put((rank, bool(torch.equal(a, ref)), bool(torch.equal(b, ref)), bool(torch.equal(loc, ref[lo:hi])),
-               bool(np.array_equal(c.numpy(), cref)), bool(np.array_equal(e.numpy(), eref)), bool(gok)))
+               bool(np.array_equal(c.numpy(), cref)), bool(np.array_equal(e.numpy(), eref)), bool(gok), bool(mh)))
     finally:
         dist.destroy_process_group()
 
