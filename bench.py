@@ -48,15 +48,24 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# Shared-memory int32 atomic throughput (lane-ops per clock per SM, conflict-free), measured
-# with tools/microbench/smem_ubench.cu on a B200.  The ALU-side roofline
-# of the histogram kernels: one red.shared per (cell or regrouped vertex, direction).
-SMEM_ATOMS_PER_CLK_SM = 16.0
+# Shared-memory int32 atomic throughput (lane-ops per clock per SM, conflict-free): the
+# ALU-side roofline of the histogram kernels (one red.shared per (cell or regrouped vertex,
+# direction)).  Read from the committed output of tools/microbench/smem_ubench.cu on a B200
+# (profiles/r02_smem_ubench.txt, line "ATOMS conflict-free ... lane-ops/clk/SM").
+def smem_atoms_per_clk():
+    p = os.path.join(ROOT, "profiles", "r02_smem_ubench.txt")
+    try:
+        for line in open(p):
+            if line.startswith("ATOMS conflict-free"):
+                return float(line.split("Gop/s")[1].split()[0]), "profiles/r02_smem_ubench.txt"
+    except OSError:
+        pass
+    raise RuntimeError("profiles/r02_smem_ubench.txt (smem_ubench output) is missing: the alu roofline needs it")
 
 
 def alu_peak(sm_mhz):
-    """Peak shared-atomic updates per second: 148 SMs x 16 lane-ops/clk x the max SM clock."""
-    return 148 * SMEM_ATOMS_PER_CLK_SM * sm_mhz * 1e6
+    """Peak shared-atomic updates per second: 148 SMs x measured lane-ops/clk x the max SM clock."""
+    return 148 * smem_atoms_per_clk()[0] * sm_mhz * 1e6
 
 
 def load_traffic(key):
@@ -417,7 +426,8 @@ def run_ours(args, rank, world, local_rank):
         achieved = work / (main_ms / 1e3) / 1e9
         roof = {"kernel": kname, "bound": "alu", "achieved": achieved, "peak": apeak / 1e9, "unit": "Gupdates/s",
                 "frac": achieved * 1e9 / apeak,
-                "peak_source": "148 SMs x 16 shared int32 atomic lane-ops/clk (tools/microbench/smem_ubench.cu) x sm_max_mhz",
+                "peak_source": f"148 SMs x {smem_atoms_per_clk()[0]:.2f} shared int32 atomic lane-ops/clk "
+                               f"(measured: {smem_atoms_per_clk()[1]}) x sm_max_mhz",
                 "work_per_launch": work,
                 "hbm_achieved_gbs": frac * wl["alg_bytes"] / per_call_launches / (main_ms / 1e3) / 1e9}
     traffic = load_traffic(f"cfg{args.config}" + (f"_D{args.D}" if args.D else ""))
@@ -522,8 +532,25 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------- the CPU oracle
+def cpu_model():
+    """The host CPU's model name (lscpu / /proc/cpuinfo) for the cpu_baseline record."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(wl, budget_s=15.0, max_units=None):
     """Time O2 (oracle/, binary64, OpenMP over directions) on a bounded sample."""
+    res = _cpu_baseline(wl, budget_s, max_units)
+    res["cpu_model"] = cpu_model()
+    return res
+
+
+def _cpu_baseline(wl, budget_s=15.0, max_units=None):
     import oracle
 
     cores = oracle.num_threads()
@@ -565,10 +592,10 @@ def cpu_baseline(wl, budget_s=15.0, max_units=None):
                 "sample": f"O2 on the explicit Freudenthal complexes of images [0, {done}) ({t:.1f} s)"}
     if wl["kind"] == "images" and wl["img"].shape[1:] == (28, 28):
         # all host cores, then one core (the paper's single-core comparison)
-        res = cpu_baseline(dict(wl, kind="images_batch"), budget_s, max_units)
+        res = _cpu_baseline(dict(wl, kind="images_batch"), budget_s, max_units)
         oracle.set_num_threads(1)
         try:
-            one = cpu_baseline(dict(wl, kind="images_batch"), min(5.0, budget_s), 200)
+            one = _cpu_baseline(dict(wl, kind="images_batch"), min(5.0, budget_s), 200)
         finally:
             oracle.set_num_threads(cores)
         res["value_1core"] = one["value"]
@@ -667,7 +694,8 @@ def run_reference(args):
             "ms_per_step": 1e3 * sum(t for t, _, _ in times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 bins / int64 sums", "data": "synthetic",
             "config": {"workload": wl["name"], "desc": wl["desc"]},
-            "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
