@@ -512,11 +512,7 @@ static wect_status run_complex(int mode, const wect_complex_desc* K, const float
   if (s != WECT_OK) return s;
   s = launch_complex_params(mode, n, m64, m32, r1, smax, *grid, gp, st);
   if (s != WECT_OK) return s;
-  if (!floatw) {
-    for (int i = 0; i < ns && s == WECT_OK; ++i)
-      if (segs.s[i].weights) s = launch_absmax_i32((const int32_t*)segs.s[i].weights, segs.s[i].count, wmax, st, nsm);
-    if (s != WECT_OK) return s;
-  }
+  // (max|w| of integer weights, where a kernel needs it, is computed inside launch_complex)
   s = launch_complex(mode, n, floatw, segs, coords, K->k0, dsrc, D, d_begin, Dc, T, gp, wmax, diff, st, nsm);
   if (s != WECT_OK) return s;
   s = launch_finalize(diff, floatw, Dc, T, ov.dev, odtype, st);

@@ -363,15 +363,38 @@ wect_status launch_complex_vb(int n, bool floatw, const Segs& segs, const float*
                               const float* dirs, int d_begin, int Dc, int T, const GridParams* gp,
                               const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms);
 
+wect_status launch_absmax_i32(const int32_t* w, int64_t n, unsigned int* out, cudaStream_t st, int num_sms);
+
+// max|w| over the integer weight arrays into the (zeroed) device word *wmax: the int32
+// partial-flush bound of k_cells / k_cells_vb / k_complex.  (k_stream checks its weights per
+// unit in-kernel instead, so the streaming path skips this pass over the weights.)
+static wect_status ensure_wmax(bool floatw, const Segs& segs, const unsigned int* wmax, cudaStream_t st,
+                               int num_sms) {
+  if (floatw) return WECT_OK;
+  for (int i = 0; i < segs.nseg; ++i)
+    if (segs.s[i].weights) {
+      const wect_status s = launch_absmax_i32((const int32_t*)segs.s[i].weights, segs.s[i].count,
+                                              const_cast<unsigned int*>(wmax), st, num_sms);
+      if (s != WECT_OK) return s;
+    }
+  return WECT_OK;
+}
+
 wect_status launch_complex(int mode, int n, bool floatw, const Segs& segs, const float* coords, int64_t k0,
                            const float* fsrc, int m_or_D, int d_begin, int Dc, int T, const GridParams* gp,
                            const unsigned int* wmax, void* diff, cudaStream_t st, int num_sms) {
   if (mode == 1 || Dc <= 3 * kCellTile) {  // ECF, or D <= 24: streaming passes (tiles of 8 filters), thread per cell
     const wect_status s = launch_stream(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp,
-                                        wmax, diff, st, num_sms);
+                                        nullptr, diff, st, num_sms);
     if (s != WECT_ENOTSUP) return s;
+    const wect_status sw = ensure_wmax(floatw, segs, wmax, st, num_sms);
+    if (sw != WECT_OK) return sw;
     return launch_cells(mode, n, floatw, segs, k0, fsrc, m_or_D, coords, fsrc, d_begin, Dc, T, gp, wmax, diff, st,
                         num_sms);
+  }
+  {
+    const wect_status sw = ensure_wmax(floatw, segs, wmax, st, num_sms);
+    if (sw != WECT_OK) return sw;
   }
   if (vb_supported(T) && !getenv("WECT_DISABLE_VB")) {  // vertex bins once per tile, cells from packed rows
     const wect_status s = launch_complex_vb(n, floatw, segs, coords, k0, fsrc, d_begin, Dc, T, gp, wmax, diff, st,

@@ -93,6 +93,7 @@ template <int MODE, int N, bool FLOATW>
 struct StreamCtx {
   using Acc = typename std::conditional<FLOATW, float, int>::type;
   const float* fv;      // MODE 0: fvals + p0
+  const uint16_t* vb;   // one filter (np == 1): its exact vertex bins (k_vbin1), gathered per cell
   int m;                // MODE 0: row stride of fvals
   const float* coords;  // MODE 1
   const float* sdir;    // MODE 1: [np][N] in shared memory
@@ -106,6 +107,23 @@ struct StreamCtx {
   Acc* hist;
 };
 
+// int32 partials are flushed every kStreamFlushCells cells per CTA, which is exact while every
+// weight added to them has |w| <= kStreamWBound; a warp whose unit holds a larger weight adds
+// that unit straight into the int64 table instead (checked per unit in-kernel, so no pre-pass
+// over the weights is needed).
+constexpr unsigned kStreamWBound = 4095;
+constexpr int64_t kStreamFlushCells = 524288;  // 524288 * 4095 < 2^31
+template <typename Acc, int CPT>
+__device__ __forceinline__ bool unit_needs_direct(const Acc (&w)[CPT]) {
+  unsigned m = 0;
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int x = (int)w[k];
+    m = max(m, (unsigned)(x < 0 ? -x : x));  // |INT_MIN| wraps to 2^31 as unsigned: > bound
+  }
+  return __reduce_max_sync(0xffffffffu, m) > kStreamWBound;
+}
+
 __device__ __noinline__ void stream_add_direct(void* diff, int64_t o, int w) {
   atomicAdd((unsigned long long*)diff + o, (unsigned long long)(long long)w);
 }
@@ -115,7 +133,8 @@ __device__ __noinline__ void stream_add_direct(void* diff, int64_t o, int w) {
 // per (cell, filter).  Near-edge cells are repaired after the fast pass (rare calls).
 template <int MODE, int N, bool FLOATW, int AR, int KG>
 __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c, const int (*v)[AR],
-                                             const typename StreamCtx<MODE, N, FLOATW>::Acc* w, int lane) {
+                                             const typename StreamCtx<MODE, N, FLOATW>::Acc* w, int lane,
+                                             bool udirect) {
   if constexpr (MODE == 0) {
     for (int pp = 0; pp < c.np; ++pp) {
       const float* fp = opaque(c.fv + pp);  // keeps each gather one IMAD.WIDE.U32 off the base
@@ -141,7 +160,7 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
         for (int k = 0; k < KG; ++k)
           if (dist[k] < c.tau) bin[k] = stream_ecf_repair(hm[k], c.gp);
       }
-      if (!FLOATW && c.direct) {
+      if (!FLOATW && (c.direct || udirect)) {
 #pragma unroll
         for (int k = 0; k < KG; ++k) stream_add_direct(c.diff, (int64_t)(c.row0 + pp) * c.T + bin[k], (int)w[k]);
       } else {
@@ -192,7 +211,7 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
             bin[k] = stream_wect_repair<N, AR>(ids, c.coords, s, c.gp);
           }
       }
-      if (!FLOATW && c.direct) {
+      if (!FLOATW && (c.direct || udirect)) {
 #pragma unroll
         for (int k = 0; k < KG; ++k) stream_add_direct(c.diff, (int64_t)(c.row0 + pp) * c.T + bin[k], (int)w[k]);
       } else {
@@ -268,7 +287,8 @@ __device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c,
   }
   if (bad) atomicOr(&g_err_word, 1u);
 #pragma unroll
-  for (int k0 = 0; k0 < CPT; k0 += KG) stream_group<MODE, N, FLOATW, AR, KG>(c, v + k0, w + k0, lane);
+  const bool udirect = !FLOATW && unit_needs_direct<Acc, CPT>(w);
+  for (int k0 = 0; k0 < CPT; k0 += KG) stream_group<MODE, N, FLOATW, AR, KG>(c, v + k0, w + k0, lane, udirect);
 }
 
 // ---- ECF with one filter per tile (MODE 0, np == 1): software-pipelined over units.
@@ -278,7 +298,7 @@ __device__ __forceinline__ void stream_unit(const StreamCtx<MODE, N, FLOATW>& c,
 template <bool FLOATW, int AR>
 __device__ __forceinline__ void ecf_read(const StreamCtx<0, 1, FLOATW>& c, const Seg& S, int64_t b0, int cells,
                                          const int* sid, const void* sw, uint64_t* empty, int ctid, int lane,
-                                         float (&h)[stream_unit_cells(AR) / (32 * kStreamConsumers)][AR],
+                                         int (&h)[stream_unit_cells(AR) / (32 * kStreamConsumers)][AR],
                                          typename StreamCtx<0, 1, FLOATW>::Acc (&w)[stream_unit_cells(AR) / (32 * kStreamConsumers)]) {
   using Acc = typename StreamCtx<0, 1, FLOATW>::Acc;
   constexpr int CPT = stream_unit_cells(AR) / (32 * kStreamConsumers);
@@ -322,37 +342,28 @@ __device__ __forceinline__ void ecf_read(const StreamCtx<0, 1, FLOATW>& c, const
     }
   }
   if (bad) atomicOr(&g_err_word, 1u);
-  const float* fp = opaque(c.fv);
+  // the cell's vertex bins (exact, k_vbin1): the cell's bin is their max (eq. msi)
 #pragma unroll
   for (int k = 0; k < CPT; ++k)
 #pragma unroll
-    for (int t = 0; t < AR; ++t) h[k][t] = __ldg(fp + (uint32_t)v[k][t] * (uint32_t)c.m);
+    for (int t = 0; t < AR; ++t) h[k][t] = (int)__ldg(c.vb + (uint32_t)v[k][t]);
 }
 
 template <bool FLOATW, int AR>
 __device__ __forceinline__ void ecf_finish(const StreamCtx<0, 1, FLOATW>& c,
-                                           const float (&h)[stream_unit_cells(AR) / (32 * kStreamConsumers)][AR],
+                                           const int (&h)[stream_unit_cells(AR) / (32 * kStreamConsumers)][AR],
                                            const typename StreamCtx<0, 1, FLOATW>::Acc (&w)[stream_unit_cells(AR) / (32 * kStreamConsumers)],
                                            int lane) {
+  using Acc = typename StreamCtx<0, 1, FLOATW>::Acc;
   constexpr int CPT = stream_unit_cells(AR) / (32 * kStreamConsumers);
-  float hm[CPT], dist[CPT], dmin = 2.f;
   int bin[CPT];
 #pragma unroll
   for (int k = 0; k < CPT; ++k) {
-    hm[k] = h[k][0];
+    bin[k] = h[k][0];
 #pragma unroll
-    for (int t = 1; t < AR; ++t) hm[k] = fmaxf(hm[k], h[k][t]);
-    const float uu = fmaf(hm[k], c.g.A, c.g.B);
-    bin[k] = max(0, min(__float2int_ru(uu), c.T - 1));
-    dist[k] = fabsf(uu - rintf(uu));
-    dmin = fminf(dmin, dist[k]);
+    for (int t = 1; t < AR; ++t) bin[k] = max(bin[k], h[k][t]);
   }
-  if (__builtin_expect(dmin < c.tau, 0)) {
-#pragma unroll
-    for (int k = 0; k < CPT; ++k)
-      if (dist[k] < c.tau) bin[k] = stream_ecf_repair(hm[k], c.gp);
-  }
-  if (!FLOATW && c.direct) {
+  if (!FLOATW && (c.direct || unit_needs_direct<Acc, CPT>(w))) {
 #pragma unroll
     for (int k = 0; k < CPT; ++k) stream_add_direct(c.diff, (int64_t)c.row0 * c.T + bin[k], (int)w[k]);
   } else {
@@ -386,7 +397,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     k_stream(Segs segs, StreamUnits su, int64_t k0, const float* __restrict__ fvals, int m,
              const float* __restrict__ coords, const float* __restrict__ dirs, int d_begin, int Dc,
              const GridParams* __restrict__ gp, int rl, const unsigned int* __restrict__ wmax_bits,
-             int64_t float_chunk, const char* __restrict__ pf, int64_t pf_bytes, void* __restrict__ diff) {
+             int64_t float_chunk, const char* __restrict__ pf, int64_t pf_bytes, const uint16_t* __restrict__ vbins,
+             void* __restrict__ diff) {
   using Acc = typename std::conditional<FLOATW, float, int>::type;
   constexpr int NS = N > 0 ? N : 1;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -470,6 +482,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   // ---- consumer warps
   StreamCtx<MODE, NS, FLOATW> c;
   c.fv = MODE == 0 ? fvals + p0 : nullptr;
+  c.vb = vbins;
   c.m = m;
   c.coords = coords;
   c.sdir = sdir;
@@ -488,17 +501,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   // flush period (units): int32 partials below 2^31 (device max|w|); float every float_chunk cells
   int64_t every_cells;
   if (FLOATW) every_cells = float_chunk;
-  else {
-    const unsigned wm = *wmax_bits;
-    every_cells = wm == 0 ? ((int64_t)1 << 62) : (int64_t)(2147483647u / wm);
-    c.direct = every_cells < 2048;  // a unit alone could overflow an int32 partial
-  }
+  else every_cells = kStreamFlushCells;  // + the per-unit weight check (unit_needs_direct)
   int64_t since = 0;
   int sg = 0;
   bool small_ar = true;  // the pipelined path keeps two units of gathers in registers: arity <= 3
   for (int i = 0; i < segs.nseg; ++i) small_ar &= ssegs[i].arity <= 3;
-  if constexpr (MODE == 0) {
-    if (np == 1 && small_ar) {
+  {
+    if (vbins != nullptr && np == 1 && small_ar) {  // one filter: gather exact vertex bins (k_vbin1)
       const StreamCtx<0, 1, FLOATW>& c1 = *reinterpret_cast<const StreamCtx<0, 1, FLOATW>*>(&c);
       int64_t j = 0;
       while (j < my_units) {
@@ -527,9 +536,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 #define WECT_ECF_AR(A)                                                                                       \
   case A: {                                                                                                  \
     constexpr int CPT = stream_unit_cells(A) / (32 * kStreamConsumers);                                     \
-    float h0[CPT][A], h1[CPT][A];                                                                            \
+    int h0[CPT][A], h1[CPT][A];                                                                              \
     Acc w0[CPT], w1[CPT];                                                                                    \
-    auto rd = [&](int64_t jj, float(&h)[CPT][A], Acc(&w)[CPT]) {                                            \
+    auto rd = [&](int64_t jj, int(&h)[CPT][A], Acc(&w)[CPT]) {                                              \
       const int st = (int)(jj % kStreamStages);                                                              \
       const int64_t bb = (blockIdx.x + jj * G - sustart[sg]) * uc;                                          \
       mbar_wait(&full[st], (unsigned)((jj / kStreamStages) & 1));                                           \
@@ -589,6 +598,67 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   stream_flush<FLOATW, Acc>(hist, np, T, rl, tile * kStreamTile, Dc, diff, tid);
 }
 
+// Exact vertex bins of ONE filter (Alg. 1 line 3, VIndices = alpha(FVals)): MODE 0 the
+// given values fvals[v * m + p0], MODE 1 the height <coords[v], s_p0> in the same fp32
+// evaluation order as k_stream (so the same guard tau applies); near-edge vertices are
+// repaired in binary64 (reading A1).  A cell's bin is then the max of its vertices' bins
+// (eq. msi: alpha is monotone), so the streaming pass gathers 2-byte bins instead
+// of filter values and bins nothing per cell.
+template <int MODE, int N>
+__device__ __forceinline__ int vbin1_one(int64_t v, const float* __restrict__ fvals, int m, int p0,
+                                         const float* __restrict__ coords, const float (&s)[N > 0 ? N : 1],
+                                         const GridParams& g, float h) {
+  constexpr int NS = N > 0 ? N : 1;
+  int b = alpha32_or_repair(h, g);
+  if (b < 0) {
+    double hd = (double)h;  // MODE 0: filter values are exact in binary64
+    if (MODE == 1) {
+      const float* x = coords + v * NS;
+      hd = __dmul_rn((double)x[0], (double)s[0]);
+      for (int i = 1; i < NS; ++i) hd = __dadd_rn(hd, __dmul_rn((double)x[i], (double)s[i]));
+    }
+    note_repair();
+    b = alpha64(hd, g);
+  }
+  return b;
+}
+
+template <int MODE, int N>
+__global__ void __launch_bounds__(256) k_vbin1(int64_t k0, const float* __restrict__ fvals, int m, int p0,
+                                               const float* __restrict__ coords, const float* __restrict__ dirs,
+                                               const GridParams* __restrict__ gp, uint16_t* __restrict__ vb) {
+  const GridParams g = *gp;
+  constexpr int NS = N > 0 ? N : 1;
+  float s[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) s[i] = MODE == 1 ? dirs[(int64_t)p0 * NS + i] : 0.f;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  // 4 consecutive vertices per thread step: one 16-byte load of filter values (MODE 0, one
+  // column, aligned) and one 8-byte store of their bins
+  const bool vec = MODE == 0 && m == 1 && p0 == 0 && ((uintptr_t)fvals & 15) == 0 && ((uintptr_t)vb & 7) == 0;
+  const int64_t n4 = vec ? k0 / 4 : 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += nt) {
+    const float4 f = __ldg((const float4*)fvals + t);
+    const float hv[4] = {f.x, f.y, f.z, f.w};
+    uint32_t b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = (uint32_t)vbin1_one<MODE, N>(4 * t + k, fvals, m, p0, coords, s, g, hv[k]);
+    *(uint2*)(vb + 4 * t) = make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
+  }
+  for (int64_t v = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < k0; v += nt) {
+    float h;
+    if (MODE == 0) {
+      h = __ldg(fvals + v * m + p0);
+    } else {
+      const float* x = coords + v * NS;
+      h = __ldg(x) * s[0];
+#pragma unroll
+      for (int i = 1; i < NS; ++i) h = fmaf(__ldg(x + i), s[i], h);
+    }
+    vb[v] = (uint16_t)vbin1_one<MODE, N>(v, fvals, m, p0, coords, s, g, h);
+  }
+}
+
 // Host side.  Returns WECT_ENOTSUP when the streaming kernel does not apply (an arity above
 // kStreamMaxAr, a misaligned list, or a histogram that does not fit); the caller then
 // uses k_cells.
@@ -602,10 +672,25 @@ static wect_status launch_stream_t(bool floatw, const Segs& segs, const StreamUn
   // the gathered array, prefetched into L2 when it fits comfortably
   const char* pf = MODE == 0 ? (const char*)fvals : (const char*)coords;
   int64_t pf_bytes = k0 * (int64_t)(MODE == 0 ? m : N) * 4;
+  // (the caller's fvals start at p0 = d_begin: k_stream indexes fvals + p0 itself)
   if (pf_bytes > ((int64_t)64 << 20) || ((uintptr_t)pf & 15)) pf_bytes = 0;
   const size_t smem = (size_t)kStreamStages * (kStreamIdxBytes + kStreamWBytes) + ((size_t)np * T * 4 << rl);
   int per_tile = num_sms / tiles;
   per_tile = per_tile < 1 ? 1 : per_tile;
+  // one filter, cells of arity <= 3: exact vertex bins first (k_vbin1), gathered per cell
+  bool small_ar = true;
+  for (int i = 0; i < segs.nseg; ++i) small_ar &= segs.s[i].arity <= 3;
+  AsyncScratch mem(st);
+  uint16_t* vb = nullptr;
+  if (Dc == 1 && small_ar && T <= 65536 && !getenv("WECT_STREAM_NO_VBIN")) {
+    WECT_CUDA_TRY(mem.alloc(&vb, (size_t)(k0 > 0 ? k0 : 1) * sizeof(uint16_t)));
+    const int vblocks = (int)((k0 + 255) / 256 < num_sms * 8 ? (k0 + 255) / 256 : num_sms * 8);
+    k_vbin1<MODE, N><<<vblocks > 0 ? vblocks : 1, 256, 0, st>>>(k0, fvals, m, d_begin, coords, dirs, gp, vb);
+    count_launch();
+    WECT_CUDA_TRY(cudaGetLastError());
+    pf = (const char*)vb;  // the gathered array is now the bins
+    pf_bytes = k0 * 2 <= ((int64_t)64 << 20) ? ((k0 * 2) & ~(int64_t)15) : 0;
+  }
   const int64_t nunits = su.ustart[segs.nseg];
   if (per_tile > nunits) per_tile = (int)(nunits > 0 ? nunits : 1);
   dim3 grid((unsigned)per_tile, (unsigned)tiles);
@@ -614,12 +699,12 @@ static wect_status launch_stream_t(bool floatw, const Segs& segs, const StreamUn
     auto k = k_stream<MODE, N, true>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, kStreamThreads, smem, st>>>(segs, su, k0, fvals, m, coords, dirs, d_begin, Dc, gp, rl, wmax, 8192,
-                                          pf, pf_bytes, diff);
+                                          pf, pf_bytes, vb, diff);
   } else {
     auto k = k_stream<MODE, N, false>;
     WECT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, kStreamThreads, smem, st>>>(segs, su, k0, fvals, m, coords, dirs, d_begin, Dc, gp, rl, wmax, 8192,
-                                          pf, pf_bytes, diff);
+                                          pf, pf_bytes, vb, diff);
   }
   count_launch();
   timer.stop();
