@@ -67,3 +67,30 @@ def test_sweep_tail_group_and_partial_chunk(w):
     for dt, T in (("int32", 12), ("int64", 20), ("int32", 8)):
         out = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs).to(DEV), T, out_dtype=dt)
         assert (out.cpu().numpy() == oracle.wect_images(img, dirs, T)).all()
+
+
+def test_one_filter_stream_without_vertex_bins_matches(w, monkeypatch):
+    """WECT_STREAM_NO_VBIN=1 sends the one-filter ECF through k_stream's per-cell binning
+    (the round-1 path): the same result as the k_vbin1 path and O2."""
+    cx = synth.torus_mesh(40, 50, 9)
+    f = np.random.default_rng(9).uniform(-1, 1, (cx.k0, 1)).astype(np.float32)
+    cells = [(torch.from_numpy(c.verts).to(DEV), torch.from_numpy(c.weights).to(DEV), c.dim) for c in cx.cells]
+    vw = torch.from_numpy(cx.vweights).to(DEV)
+    a = w.ecf_complex(torch.from_numpy(f).to(DEV), cells, 128, vweights=vw).cpu().numpy()
+    monkeypatch.setenv("WECT_STREAM_NO_VBIN", "1")
+    b = w.ecf_complex(torch.from_numpy(f).to(DEV), cells, 128, vweights=vw).cpu().numpy()
+    ref = oracle.ecf_complex(cx, f, 128)
+    assert (a == ref).all() and (b == ref).all()
+
+
+def test_stream_large_weights_take_the_direct_path(w):
+    """Integer weights above the in-kernel bound (|w| > 4095) make a warp add its unit straight
+    into the int64 table: exact, no max|w| pre-pass."""
+    cx = synth.torus_mesh(40, 50, 10)
+    g = np.random.default_rng(10)
+    for c in cx.cells:
+        c.weights[:] = g.integers(-2**30, 2**30, c.weights.shape[0]).astype(np.int32)
+    f = g.uniform(-1, 1, (cx.k0, 1)).astype(np.float32)
+    cells = [(torch.from_numpy(c.verts).to(DEV), torch.from_numpy(c.weights).to(DEV), c.dim) for c in cx.cells]
+    got = w.ecf_complex(torch.from_numpy(f).to(DEV), cells, 64, vweights=torch.from_numpy(cx.vweights).to(DEV))
+    assert (got.cpu().numpy() == oracle.ecf_complex(cx, f, 64)).all()
