@@ -33,28 +33,33 @@
 namespace wect {
 
 constexpr int kRecRows = 15;     // vertex rows per 32-byte record (u16 header + 15 u16 rows)
-constexpr int kSweepWarps = 16;
+constexpr int kSweepWarps = 32;   // two per direction: the bins below / above its split
 constexpr int kSweepImgs = 64;   // images per CTA group: lane l owns images l, l + 32
 constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
 constexpr int kStageRow = 32;    // bytes per image row of an output chunk (8 int32 / 4 int64 bins)
 constexpr int kStageBytes = kSweepImgs * kStageRow;  // per warp
 constexpr int kRingRecs = 32;    // per-warp record ring: two halves of 16 records (32 B each)
 constexpr int kRingBytes = kRingRecs * 32;  // 1 KB: halves at byte 0 and 512 (ro >> 9)
-constexpr int kSweepMaxHW = 1000;
+constexpr int kSweepMaxHW = 1024;
 
 __host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
 // bins per output chunk for an output element of osz bytes (64-byte image rows)
 __host__ __device__ constexpr int chunk_bins(int osz) { return kStageRow / osz; }
 // 32-byte records per direction: one per bin at least, + one per 15 vertices, + the prefetch pad
 __host__ __device__ constexpr int sweep_rec_stride(int HW, int Tp) { return Tp + (HW + kRecRows - 1) / kRecRows + 8; }
-// smem of k_sweep2d: cw table [HW][128 B] (1024-aligned) | output stages [16][2 KB] |
-// record rings [16][1 KB] | ring mbarriers [16][2] | pixels [HW][68 B]
+// smem of k_sweep2d: cw table [HW][128 B] (1024-aligned) | output stages [32][2 KB] |
+// record rings [32][1 KB] | ring mbarriers [32][2] | image totals [32 words][2].  The
+// staged pixels [HW][68 B] overlay the stages + rings: they are only read by the cw build,
+// before any sweep of the phase uses its stage or ring.
 __host__ __device__ constexpr size_t sweep_cw_bytes(int HW) { return align_up((size_t)HW * 128, 1024); }
 __host__ __device__ constexpr size_t sweep_fixed_bytes() {
-  return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16);
+  return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16) + 256;
 }
 __host__ __device__ constexpr size_t sweep_smem_bytes(int HW) {
-  return 1024 + sweep_cw_bytes(HW) + sweep_fixed_bytes() + align_up((size_t)HW * kPixStride, 16);
+  return 1024 + sweep_cw_bytes(HW) + sweep_fixed_bytes();
+}
+__host__ __device__ constexpr bool sweep_pix_fits(int HW) {
+  return (size_t)HW * kPixStride <= (size_t)kSweepWarps * (kStageBytes + kRingBytes);
 }
 
 // Freudenthal designated vertex (offset index: 0 self, 1 X = (r,c+1), 2 Y = (r+1,c),
@@ -103,7 +108,7 @@ __host__ __device__ __forceinline__ int rec_slot(int n, int p) {
 __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __restrict__ dirs, int d_begin, int Dc,
                                                 const GridParams* __restrict__ gp, uint4* __restrict__ recs,
                                                 int rec_stride, int Tp, int* __restrict__ qlist,
-                                                int* __restrict__ qcount, int* __restrict__ nrecs, int freud,
+                                                int* __restrict__ qcount, int4* __restrict__ split, int freud,
                                                 int4* __restrict__ corr, int* __restrict__ ncorr, int corr_cap) {
   // smem: counts[Tp], rbase[Tp], totals[Tp], vbin[HW] (u16)
   extern __shared__ int sh[];
@@ -113,6 +118,7 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
   int* rbase = sh + Tp;
   int* totals = sh + 2 * Tp;
   uint16_t* vbin = (uint16_t*)(sh + 3 * Tp);
+  __shared__ int sh_split, sh_nl, sh_tot;
   // rows in record j of a bin of c rows
   auto counts_total_rows = [&](int q, int j) {
     const int c = totals[q] - j * kRecRows;
@@ -146,10 +152,38 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
     }
     int base = incl - s;
     for (int q = q0; q < q0 + per && q < Tp; ++q) {
-      rbase[q] = base;
+      rbase[q] = base;  // ascending exclusive scan E(q) for now
       base += counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1;
     }
-    if (lane == 31) nrecs[dl] = incl;  // records of this direction's program
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    // split bin (a multiple of the 8-bin output chunk): the lower warp sweeps [0, sb) upward,
+    // the upper warp [sb, Tp) downward; balanced on ~3.5 instructions per row + ~22 per record
+    if (lane == 0) {
+      int wtot = 0;
+      for (int q = 0; q < Tp; ++q) wtot += 7 * counts[q] + 44 * (counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1);
+      int sb = 0, acc = 0, best = wtot;
+      for (int c = 0; c <= Tp; c += 8) {
+        const int d = abs(2 * acc - wtot);
+        if (d < best) { best = d; sb = c; }
+        for (int q = c; q < c + 8 && q < Tp; ++q)
+          acc += 7 * counts[q] + 44 * (counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1);
+      }
+      const int nl = sb < Tp ? rbase[sb] : tot;
+      split[dl] = make_int4(nl, tot - nl, sb, 0);
+      sh_split = sb;
+      sh_nl = nl;
+      sh_tot = tot;
+    }
+    __syncwarp();
+    // records of the upper program run from the top bin down: bin q >= sb starts at
+    // nl + (records of the bins above q)
+    const int sb = sh_split, nl = sh_nl;
+    for (int q = q0; q < q0 + per && q < Tp; ++q)
+      if (q >= sb) {
+        const int nr = counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1;
+        rbase[q] = nl + tot - rbase[q] - nr;
+      }
     if (lane == 0) {
       // cubical: quadrant (s_x > 0) | (s_y > 0) << 1; Freudenthal: chamber | (s_x + s_y > 0) << 2
       const int o = (sx > 0.f ? 1 : 0) | (sy > 0.f ? 2 : 0) | ((freud && sx + sy > 0.f) ? 4 : 0);
@@ -269,16 +303,22 @@ __device__ __forceinline__ void ring_fill(const Ring& R, int h, const uint4* pro
   bulk_g2s_plain(R.buf + h * (kRingBytes / 2), prog + 2 * first, (unsigned)n * 32u, R.bar + h);
 }
 
-// One warp, one direction, the CTA's 64 images: run the direction's record program.
-// lane_s = shared address of this lane's word of cw row 0 (row v at lane_s + 128 v); running
-// totals (B0, B1) of images (img0 + lane, img0 + lane + 32); chunk stage st (this warp's).
-template <typename OutT, bool TMA>
-__device__ __forceinline__ void sweep_direction(uint32_t lane_s, const uint4* __restrict__ prog, int nrec, Ring& R,
-                                                uint8_t* __restrict__ st, const CUtensorMap* tmap,
-                                                OutT* __restrict__ out, int64_t B, int64_t img0, int Dc, int dl,
-                                                int T, int Tp, int lane) {
+// One warp, one half of one direction, the CTA's 64 images: run the half's record program.
+// DOWN = false: bins [q_lo, q_hi) upward, the running total is the cumulative sum of the
+// rows seen (Alg. 1 line 11).  DOWN = true: bins [q_lo, q_hi) from the top down, the running
+// total R sums the rows of the bins ABOVE the current one and the emitted value is
+// total - R -- the same cumulative sum, since total = sum of every cw row = chi of the image
+// (top bin), so neither half waits for the other.  lane_s = shared address of this lane's
+// word of cw row 0 (row v at lane_s + 128 v); totals (t0, t1) of images (img0 + lane,
+// img0 + lane + 32); chunk stage st (this warp's).
+template <typename OutT, bool TMA, bool DOWN>
+__device__ __forceinline__ void sweep_half(uint32_t lane_s, const uint4* __restrict__ prog, int nrec, Ring& R,
+                                           uint8_t* __restrict__ st, const CUtensorMap* tmap, OutT* __restrict__ out,
+                                           int64_t B, int64_t img0, int Dc, int dl, int T, int q_lo, int q_hi,
+                                           int t0, int t1, int lane) {
   constexpr int CB = chunk_bins((int)sizeof(OutT));
   constexpr int PER = 16 / (int)sizeof(OutT);  // bins per 16-byte chunk
+  if (q_lo >= q_hi) return;
   if (lane == 0) {
     ring_fill(R, 0, prog, 0, nrec);
     ring_fill(R, 1, prog, 16, nrec);
@@ -288,46 +328,64 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane_s, const uint4* __
   int fill = 32;     // first record of the next refill
   int B0 = 0, B1 = 0;
   const uint32_t st_s = smem_u32(st);
+  // the rows of one bin: all its records, folded onto (B0, B1)
+  auto take_bin = [&]() {
+    uint32_t more;
+    do {
+      if ((ro & (kRingBytes / 2 - 1)) == 0) {  // entering a ring half
+        const int h = (int)(ro >> 9);
+        mbar_wait(R.bar + h, (R.ph >> h) & 1u);
+        R.ph ^= 1u << h;
+      }
+      uint4 a, b;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(ring_s + ro));
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(ring_s + ro + 16));
+      ro = (ro + 32u) & (kRingBytes - 1);
+      if ((ro & (kRingBytes / 2 - 1)) == 0 && fill < nrec) {  // left a half: refill it 32 records ahead
+        __syncwarp();
+        if (lane == 0) ring_fill(R, (int)(ro >> 9) ^ 1, prog, fill, nrec);
+        fill += 16;
+      }
+      // the header is the same in every lane: a warp reduction tells the compiler so (uniform
+      // branches, no reconvergence barriers around the row blocks)
+      const uint32_t hdr = __reduce_or_sync(0xffffffffu, a.x);
+      const uint32_t n = hdr & 15u;
+      more = hdr & 16u;
+      uint32_t S = 0;
+      if (n & 8u)
+        S = lds32(row_hi(lane_s, a.x)) + lds32(row_lo(lane_s, a.y)) + lds32(row_hi(lane_s, a.y)) +
+            lds32(row_lo(lane_s, a.z)) + lds32(row_hi(lane_s, a.z)) + lds32(row_lo(lane_s, a.w)) +
+            lds32(row_hi(lane_s, a.w)) + lds32(row_lo(lane_s, b.x));
+      if (n & 4u)
+        S += lds32(row_hi(lane_s, b.x)) + lds32(row_lo(lane_s, b.y)) + lds32(row_hi(lane_s, b.y)) +
+             lds32(row_lo(lane_s, b.z));
+      if (n & 2u) S += lds32(row_hi(lane_s, b.z)) + lds32(row_lo(lane_s, b.w));
+      if (n & 1u) S += lds32(row_hi(lane_s, b.w));
+      // signed packed pair S = s0 + s1 2^16 (mod 2^32), |s0|, |s1| <= 15 * 765
+      const int s0 = (int)(int16_t)(S & 0xFFFFu);
+      B0 += s0;
+      B1 += ((int)S - s0) >> 16;
+    } while (more);
+  };
+  const int nchunk = (q_hi - q_lo) / CB;
 #pragma unroll 1
-  for (int q0 = 0; q0 < Tp; q0 += CB) {
+  for (int ci = 0; ci < nchunk; ++ci) {
+    const int q0 = DOWN ? q_hi - (ci + 1) * CB : q_lo + ci * CB;
     int o0[CB], o1[CB];
+    if (!DOWN) {
 #pragma unroll
-    for (int k = 0; k < CB; ++k) {
-      uint32_t more;
-      do {
-        if ((ro & (kRingBytes / 2 - 1)) == 0) {  // entering a ring half
-          const int h = (int)(ro >> 9);
-          mbar_wait(R.bar + h, (R.ph >> h) & 1u);
-          R.ph ^= 1u << h;
-        }
-        uint4 a, b;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(ring_s + ro));
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(ring_s + ro + 16));
-        ro = (ro + 32u) & (kRingBytes - 1);
-        if ((ro & (kRingBytes / 2 - 1)) == 0 && fill < nrec) {  // left a half: refill it 32 records ahead
-          __syncwarp();
-          if (lane == 0) ring_fill(R, (int)(ro >> 9) ^ 1, prog, fill, nrec);
-          fill += 16;
-        }
-        const uint32_t n = a.x & 15u;
-        more = a.x & 16u;
-        uint32_t S = 0;
-        if (n & 8u)
-          S = lds32(row_hi(lane_s, a.x)) + lds32(row_lo(lane_s, a.y)) + lds32(row_hi(lane_s, a.y)) +
-              lds32(row_lo(lane_s, a.z)) + lds32(row_hi(lane_s, a.z)) + lds32(row_lo(lane_s, a.w)) +
-              lds32(row_hi(lane_s, a.w)) + lds32(row_lo(lane_s, b.x));
-        if (n & 4u)
-          S += lds32(row_hi(lane_s, b.x)) + lds32(row_lo(lane_s, b.y)) + lds32(row_hi(lane_s, b.y)) +
-               lds32(row_lo(lane_s, b.z));
-        if (n & 2u) S += lds32(row_hi(lane_s, b.z)) + lds32(row_lo(lane_s, b.w));
-        if (n & 1u) S += lds32(row_hi(lane_s, b.w));
-        // signed packed pair S = s0 + s1 2^16 (mod 2^32), |s0|, |s1| <= 15 * 765
-        const int s0 = (int)(int16_t)(S & 0xFFFFu);
-        B0 += s0;
-        B1 += ((int)S - s0) >> 16;
-      } while (more);
-      o0[k] = B0;
-      o1[k] = B1;
+      for (int k = 0; k < CB; ++k) {
+        take_bin();
+        o0[k] = B0;
+        o1[k] = B1;
+      }
+    } else {
+#pragma unroll
+      for (int k = CB - 1; k >= 0; --k) {
+        o0[k] = t0 - B0;  // rows of the bins above k only
+        o1[k] = t1 - B1;
+        take_bin();
+      }
     }
     // the previous chunk's TMA store has finished reading the stage
     if (TMA && lane == 0) tma_wait_read_all();
@@ -360,25 +418,29 @@ __device__ __forceinline__ void sweep_direction(uint32_t lane_s, const uint4* __
       __syncwarp();
     }
   }
-  __syncwarp();  // all lanes are done with the ring before the next direction refills it
+  // the stage and ring are reused (and overlaid by the next phase's pixels): reads done
+  if (TMA && lane == 0) tma_wait_read_all();
+  __syncwarp();
 }
 
 template <typename OutT, bool FREUD, bool TMA>
 __global__ void __launch_bounds__(kSweepWarps * 32, 1)
     k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint4* __restrict__ recs, int rec_stride,
-              const int* __restrict__ qlist, const int* __restrict__ qcount, const int* __restrict__ nrecs, int Dc,
+              const int* __restrict__ qlist, const int* __restrict__ qcount, const int4* __restrict__ split, int Dc,
               int T, int Tp, OutT* __restrict__ out, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // 1024-aligned (the 64B-swizzle pattern of the TMA stores), kept in the shared window
+  // 1024-aligned (the swizzle pattern of the TMA stores), kept in the shared window
   unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   const int HW = H * W;
   uint32_t* cwb = (uint32_t*)smem;  // [HW][32] words: images (j, j+32) signed packed
   uint8_t* stages = smem + sweep_cw_bytes(HW);
   uint8_t* rings = stages + kSweepWarps * kStageBytes;
   uint64_t* bars = (uint64_t*)(rings + kSweepWarps * kRingBytes);
-  uint8_t* pix = (uint8_t*)(bars + 2 * kSweepWarps);  // [HW][kPixStride] u8: byte 2j + h = image j + 32 h
+  int* totals = (int*)(bars + 2 * kSweepWarps);  // [32 lanes][2]: chi of images (lane, lane + 32)
+  uint8_t* pix = stages;  // [HW][kPixStride] u8, overlays the stages + rings: byte 2j + h = image j + 32 h
   const int lane = threadIdx.x & 31;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int half = warp & 1, wpair = warp >> 1;
   uint8_t* st = stages + warp * kStageBytes;
   Ring ring{rings + warp * kRingBytes, bars + 2 * warp, 0u};
   if (threadIdx.x < 2 * kSweepWarps) mbar_init(bars + threadIdx.x, 1);
@@ -387,6 +449,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   const uint32_t lane_s = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
   constexpr int NPH = FREUD ? 8 : 4;  // phase (quadrant / chamber) slots
+  constexpr int NPAIR = kSweepWarps / 2;
   const bool phase_split = (int)gridDim.y >= NPH;
   const int ysub = phase_split ? (int)blockIdx.y / NPH : (int)blockIdx.y;
   const int nsub = phase_split ? (int)gridDim.y / NPH : (int)gridDim.y;
@@ -394,25 +457,6 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t img0 = grp * kSweepImgs;
     const int nimg = (int)((B - img0) < kSweepImgs ? (B - img0) : kSweepImgs);
-    __syncthreads();  // the previous group's sweeps are done with pix / cwb
-    // stage the group's pixels transposed: image i -> byte 2 (i % 32) + i / 32 of pix[v]
-    if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
-      const int per = HW >> 4;
-      for (int f = threadIdx.x; f < kSweepImgs * per; f += blockDim.x) {
-        const int i = f & (kSweepImgs - 1), v = (f >> 6) << 4;
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (i < nimg) x = __ldcs((const uint4*)(img + (img0 + i) * HW + v));
-        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-        const int pos = 2 * (i & 31) + (i >> 5);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) pix[(v + k) * kPixStride + pos] = (uint8_t)(wv[k >> 2] >> (8 * (k & 3)));
-      }
-    } else {
-      for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
-        const int i = f & (kSweepImgs - 1), v = f >> 6;
-        pix[v * kPixStride + 2 * (i & 31) + (i >> 5)] = i < nimg ? img[(img0 + i) * HW + v] : (uint8_t)0;
-      }
-    }
 #pragma unroll 1
     for (int o = 0; o < NPH; ++o) {
       const int qco = qcount[o];
@@ -420,11 +464,30 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       // gridDim.y >= the phase count (then by direction within the phase), else by direction
       if (phase_split && (int)blockIdx.y % NPH != o) continue;
       if (ysub >= qco) continue;
-      __syncthreads();  // pix staged / previous phase's sweeps done with cwb
-      int v = threadIdx.x >> 5;
-      int r = v / W, c = v - r * W;
-      const int step_r = kSweepWarps / W, step_c = kSweepWarps - step_r * W;
+      __syncthreads();  // previous phase's sweeps are done with cwb, the stages and the rings
+      // stage the group's pixels transposed: image i -> byte 2 (i % 32) + i / 32 of pix[v]
+      if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
+        const int per = HW >> 4;
+        for (int f = threadIdx.x; f < kSweepImgs * per; f += blockDim.x) {
+          const int i = f & (kSweepImgs - 1), v = (f >> 6) << 4;
+          uint4 x = make_uint4(0, 0, 0, 0);
+          if (i < nimg) x = __ldg((const uint4*)(img + (img0 + i) * HW + v));
+          const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+          const int pos = 2 * (i & 31) + (i >> 5);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) pix[(v + k) * kPixStride + pos] = (uint8_t)(wv[k >> 2] >> (8 * (k & 3)));
+        }
+      } else {
+        for (int f = threadIdx.x; f < kSweepImgs * HW; f += blockDim.x) {
+          const int i = f & (kSweepImgs - 1), v = f >> 6;
+          pix[v * kPixStride + 2 * (i & 31) + (i >> 5)] = i < nimg ? img[(img0 + i) * HW + v] : (uint8_t)0;
+        }
+      }
+      __syncthreads();
       if (FREUD) {
+        int v = warp;
+        int r = v / W, c = v - r * W;
+        const int step_r = kSweepWarps / W, step_c = kSweepWarps - step_r * W;
         for (; v < HW; v += kSweepWarps) {
           cwb[v * 32 + lane] = freud_cw(pix + v * kPixStride + 2 * lane, r, c, H, W, o & 1, (o >> 1) & 1, (o >> 2) & 1);
           r += step_r;
@@ -469,10 +532,38 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
         }
       }
       __syncthreads();
-      for (int k = ysub + warp * nsub; k < qco; k += kSweepWarps * nsub) {
+      // totals: every cell is counted once in the cw table of ANY phase, so the sum of all cw
+      // rows is the image's weighted Euler characteristic (the top bin of every direction)
+      {
+        uint32_t S = 0;
+        for (int v = warp; v < HW; v += kSweepWarps) S += cwb[v * 32 + lane];  // <= 32 rows: no carry
+        const int s0 = (int)(int16_t)(S & 0xFFFFu);
+        int* red = (int*)stages;  // [32 warps][32 lanes][2], the pixels are no longer needed
+        red[(warp * 32 + lane) * 2] = s0;
+        red[(warp * 32 + lane) * 2 + 1] = ((int)S - s0) >> 16;
+        __syncthreads();
+        if (warp == 0) {
+          int a0 = 0, a1 = 0;
+          for (int w2 = 0; w2 < kSweepWarps; ++w2) {
+            a0 += red[(w2 * 32 + lane) * 2];
+            a1 += red[(w2 * 32 + lane) * 2 + 1];
+          }
+          totals[2 * lane] = a0;
+          totals[2 * lane + 1] = a1;
+        }
+        __syncthreads();
+      }
+      const int t0 = totals[2 * lane], t1 = totals[2 * lane + 1];
+      for (int k = ysub + wpair * nsub; k < qco; k += NPAIR * nsub) {
         const int dl = __shfl_sync(0xffffffffu, qlist[o * Dc + k], 0);
-        sweep_direction<OutT, TMA>(lane_s, recs + (int64_t)dl * rec_stride * 2, nrecs[dl], ring, st, &tmap, out, B,
-                                   img0, Dc, dl, T, Tp, lane);
+        const int4 sp = split[dl];  // (records below, records above, split bin)
+        const uint4* prog = recs + (int64_t)dl * rec_stride * 2;
+        if (half == 0)
+          sweep_half<OutT, TMA, false>(lane_s, prog, sp.x, ring, st, &tmap, out, B, img0, Dc, dl, T, 0, sp.z, t0, t1,
+                                       lane);
+        else
+          sweep_half<OutT, TMA, true>(lane_s, prog + 2 * sp.x, sp.y, ring, st, &tmap, out, B, img0, Dc, dl, T, sp.z,
+                                      Tp, t0, t1, lane);
       }
     }
   }
@@ -542,13 +633,15 @@ static bool make_out_map(CUtensorMap* m, void* out, int64_t B, int Dc, int T, in
 bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
   if (ndim != 2) return false;
   const int64_t HW = dims[0] * dims[1];
-  return HW >= 1 && HW <= kSweepMaxHW && T <= 4096 && sweep_smem_bytes((int)HW) <= 227 * 1024;
+  return HW >= 1 && HW <= kSweepMaxHW && T <= 4096 && sweep_smem_bytes((int)HW) <= 227 * 1024 &&
+         sweep_pix_fits((int)HW);
 }
 
 static int padded_bins(int T) { return (T + 7) & ~7; }  // a whole number of chunks for int32 and int64
 
 size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud) {
-  return (size_t)Dc * sweep_rec_stride(HW, padded_bins(T)) * 32 + 64 + (size_t)(8 + 9 * Dc + 1) * 4 + 64 +
+  return (size_t)Dc * sweep_rec_stride(HW, padded_bins(T)) * 32 + 64 + (size_t)(8 + 8 * Dc + 1) * 4 + 64 +
+         (size_t)Dc * 16 + 16 +
          (freud ? (size_t)5 * HW * Dc * sizeof(int4) + 16 : 0);
 }
 
@@ -562,8 +655,8 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   int* ints = (int*)align_up((uintptr_t)(recs + (size_t)Dc * rstride * 2), 16);
   int* qcount = ints;           // 8 chamber slots (cubical uses 4)
   int* qlist = ints + 8;        // [8][Dc]
-  int* nrecs = qlist + 8 * Dc;  // [Dc]
-  int* ncorr = nrecs + Dc;
+  int4* split = (int4*)align_up((uintptr_t)(qlist + 8 * Dc), 16);  // [Dc]
+  int* ncorr = (int*)(split + Dc);
   int4* corr = (int4*)align_up((uintptr_t)(ncorr + 1), 16);
   const int corr_cap = freud ? 5 * HW * Dc : 0;
   WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 8 * sizeof(int), st));
@@ -571,7 +664,7 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   const size_t sort_smem = (size_t)3 * Tp * sizeof(int) + align_up((size_t)HW * 2, 16);
   if (sort_smem > 48 * 1024)
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sort2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
-  k_sort2d<<<Dc, 256, sort_smem, st>>>(H, W, dirs, d_begin, Dc, gp, recs, rstride, Tp, qlist, qcount, nrecs, freud,
+  k_sort2d<<<Dc, 256, sort_smem, st>>>(H, W, dirs, d_begin, Dc, gp, recs, rstride, Tp, qlist, qcount, split, freud,
                                        corr, ncorr, corr_cap);
   count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
@@ -579,10 +672,10 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   const int64_t ngroups = (B + kSweepImgs - 1) / kSweepImgs;
   // fewer image groups than SMs (small batches): split every phase's directions over CTAs
   const int nph = freud ? 8 : 4;
-  int split = (int)(num_sms / (ngroups > 0 ? ngroups : 1));
-  split = split < 1 ? 1 : (split > kSweepWarps * nph ? kSweepWarps * nph : split);
-  if (split >= nph) split = (split / nph) * nph;  // whole phase rows: y = phase + nph * sub
-  const dim3 grid((unsigned)(ngroups < num_sms ? ngroups : num_sms), (unsigned)split);
+  int ysplit = (int)(num_sms / (ngroups > 0 ? ngroups : 1));
+  ysplit = ysplit < 1 ? 1 : (ysplit > (kSweepWarps / 2) * nph ? (kSweepWarps / 2) * nph : ysplit);
+  if (ysplit >= nph) ysplit = (ysplit / nph) * nph;  // whole phase rows: y = phase + nph * sub
+  const dim3 grid((unsigned)(ngroups < num_sms ? ngroups : num_sms), (unsigned)ysplit);
   const int osz = odtype == WECT_I32 ? 4 : 8;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -591,7 +684,7 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
 #define WECT_SWEEP(OT, FR, TM)                                                                                      \
   do {                                                                                                              \
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<OT, FR, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_sweep2d<OT, FR, TM><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, recs, rstride, qlist, qcount, nrecs, Dc, T, \
+    k_sweep2d<OT, FR, TM><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, recs, rstride, qlist, qcount, split, Dc, T, \
                                                                  Tp, (OT*)out, tmap);                                   \
     count_launch();                                                                                                 \
   } while (0)
