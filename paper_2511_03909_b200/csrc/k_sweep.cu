@@ -49,8 +49,9 @@ __host__ __device__ constexpr int chunk_bins(int osz) { return kStageRow / osz; 
 __host__ __device__ constexpr int sweep_rec_stride(int HW, int Tp) { return Tp + (HW + kRecRows - 1) / kRecRows + 8; }
 // smem of k_sweep2d: cw table [HW][128 B] (1024-aligned) | output stages [32][2 KB] |
 // record rings [32][1 KB] | ring mbarriers [32][2] | image totals [32 words][2].  The
-// staged pixels [HW][68 B] overlay the stages + rings: they are only read by the cw build,
-// before any sweep of the phase uses its stage or ring.
+// staged pixels [HW][68 B] overlay the stages: they are only read by the cw build, before
+// any sweep of the phase uses its stage (the rings stay free, so every warp starts loading
+// its program while the CTA stages pixels and builds cw).
 __host__ __device__ constexpr size_t sweep_cw_bytes(int HW) { return align_up((size_t)HW * 128, 1024); }
 __host__ __device__ constexpr size_t sweep_fixed_bytes() {
   return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16) + 256;
@@ -59,7 +60,7 @@ __host__ __device__ constexpr size_t sweep_smem_bytes(int HW) {
   return 1024 + sweep_cw_bytes(HW) + sweep_fixed_bytes();
 }
 __host__ __device__ constexpr bool sweep_pix_fits(int HW) {
-  return (size_t)HW * kPixStride <= (size_t)kSweepWarps * (kStageBytes + kRingBytes);
+  return (size_t)HW * kPixStride <= (size_t)kSweepWarps * kStageBytes;
 }
 
 // Freudenthal designated vertex (offset index: 0 self, 1 X = (r,c+1), 2 Y = (r+1,c),
@@ -315,36 +316,40 @@ template <typename OutT, bool TMA, bool DOWN>
 __device__ __forceinline__ void sweep_half(uint32_t lane_s, const uint4* __restrict__ prog, int nrec, Ring& R,
                                            uint8_t* __restrict__ st, const CUtensorMap* tmap, OutT* __restrict__ out,
                                            int64_t B, int64_t img0, int Dc, int dl, int T, int q_lo, int q_hi,
-                                           int t0, int t1, int lane) {
+                                           int t0, int t1, int lane, bool prefilled) {
   constexpr int CB = chunk_bins((int)sizeof(OutT));
   constexpr int PER = 16 / (int)sizeof(OutT);  // bins per 16-byte chunk
   if (q_lo >= q_hi) return;
-  if (lane == 0) {
+  if (lane == 0 && !prefilled) {
     ring_fill(R, 0, prog, 0, nrec);
     ring_fill(R, 1, prog, 16, nrec);
   }
   const uint32_t ring_s = smem_u32(R.buf);
   uint32_t ro = 0;   // byte offset of the next record in the ring (32 records of 32 B)
   int fill = 32;     // first record of the next refill
+  int used = 0;      // records consumed
   int B0 = 0, B1 = 0;
   const uint32_t st_s = smem_u32(st);
+  mbar_wait(R.bar, R.ph & 1u);  // the first half
+  R.ph ^= 1u;
   // the rows of one bin: all its records, folded onto (B0, B1)
   auto take_bin = [&]() {
     uint32_t more;
     do {
-      if ((ro & (kRingBytes / 2 - 1)) == 0) {  // entering a ring half
-        const int h = (int)(ro >> 9);
-        mbar_wait(R.bar + h, (R.ph >> h) & 1u);
-        R.ph ^= 1u << h;
-      }
       uint4 a, b;
       asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(ring_s + ro));
       asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(ring_s + ro + 16));
       ro = (ro + 32u) & (kRingBytes - 1);
-      if ((ro & (kRingBytes / 2 - 1)) == 0 && fill < nrec) {  // left a half: refill it 32 records ahead
+      ++used;
+      if ((ro & (kRingBytes / 2 - 1)) == 0) {  // crossed into the other half (every 16 records)
         __syncwarp();
-        if (lane == 0) ring_fill(R, (int)(ro >> 9) ^ 1, prog, fill, nrec);
+        if (lane == 0 && fill < nrec) ring_fill(R, (int)(ro >> 9) ^ 1, prog, fill, nrec);  // refill 32 ahead
         fill += 16;
+        if (used < nrec) {
+          const int h = (int)(ro >> 9);
+          mbar_wait(R.bar + h, (R.ph >> h) & 1u);
+          R.ph ^= 1u << h;
+        }
       }
       // the header is the same in every lane: a warp reduction tells the compiler so (uniform
       // branches, no reconvergence barriers around the row blocks)
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   uint8_t* rings = stages + kSweepWarps * kStageBytes;
   uint64_t* bars = (uint64_t*)(rings + kSweepWarps * kRingBytes);
   int* totals = (int*)(bars + 2 * kSweepWarps);  // [32 lanes][2]: chi of images (lane, lane + 32)
-  uint8_t* pix = stages;  // [HW][kPixStride] u8, overlays the stages + rings: byte 2j + h = image j + 32 h
+  uint8_t* pix = stages;  // [HW][kPixStride] u8, overlays the stages: byte 2j + h = image j + 32 h
   const int lane = threadIdx.x & 31;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int half = warp & 1, wpair = warp >> 1;
@@ -457,6 +462,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t img0 = grp * kSweepImgs;
     const int nimg = (int)((B - img0) < kSweepImgs ? (B - img0) : kSweepImgs);
+    bool need_tot = true;
 #pragma unroll 1
     for (int o = 0; o < NPH; ++o) {
       const int qco = qcount[o];
@@ -464,7 +470,21 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       // gridDim.y >= the phase count (then by direction within the phase), else by direction
       if (phase_split && (int)blockIdx.y % NPH != o) continue;
       if (ysub >= qco) continue;
-      __syncthreads();  // previous phase's sweeps are done with cwb, the stages and the rings
+      // this warp's first half-direction of the phase: start streaming its program now, so the
+      // first records arrive while the CTA stages pixels and builds cw
+      const int kfirst = ysub + wpair * nsub;
+      if (kfirst < qco && lane == 0) {
+        const int dl0 = qlist[o * Dc + kfirst];
+        const int4 sp0 = split[dl0];
+        const uint4* prog0 = recs + (int64_t)dl0 * rec_stride * 2 + (half ? 2 * sp0.x : 0);
+        const int nrec0 = half ? sp0.y : sp0.x;
+        const bool live = half ? sp0.z < Tp : sp0.z > 0;
+        if (live) {
+          ring_fill(ring, 0, prog0, 0, nrec0);
+          ring_fill(ring, 1, prog0, 16, nrec0);
+        }
+      }
+      __syncthreads();  // previous phase's sweeps are done with cwb and the stages
       // stage the group's pixels transposed: image i -> byte 2 (i % 32) + i / 32 of pix[v]
       if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
         const int per = HW >> 4;
@@ -533,8 +553,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
       }
       __syncthreads();
       // totals: every cell is counted once in the cw table of ANY phase, so the sum of all cw
-      // rows is the image's weighted Euler characteristic (the top bin of every direction)
-      {
+      // rows is the image's weighted Euler characteristic (the top bin of every direction):
+      // computed in the group's first phase only
+      if (need_tot) {
+        need_tot = false;
         uint32_t S = 0;
         for (int v = warp; v < HW; v += kSweepWarps) S += cwb[v * 32 + lane];  // <= 32 rows: no carry
         const int s0 = (int)(int16_t)(S & 0xFFFFu);
@@ -558,12 +580,13 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
         const int dl = __shfl_sync(0xffffffffu, qlist[o * Dc + k], 0);
         const int4 sp = split[dl];  // (records below, records above, split bin)
         const uint4* prog = recs + (int64_t)dl * rec_stride * 2;
+        const bool pre = k == kfirst;
         if (half == 0)
           sweep_half<OutT, TMA, false>(lane_s, prog, sp.x, ring, st, &tmap, out, B, img0, Dc, dl, T, 0, sp.z, t0, t1,
-                                       lane);
+                                       lane, pre);
         else
           sweep_half<OutT, TMA, true>(lane_s, prog + 2 * sp.x, sp.y, ring, st, &tmap, out, B, img0, Dc, dl, T, sp.z,
-                                      Tp, t0, t1, lane);
+                                      Tp, t0, t1, lane, pre);
       }
     }
   }
