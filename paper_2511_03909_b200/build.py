@@ -13,6 +13,8 @@ LIB = os.path.join(HERE, "libwect.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
+# extra nvcc flags for A/B experiments only (e.g. -D switches); empty in normal builds
+FLAGS += os.environ.get("WECT_NVCC_EXTRA", "").split()
 
 
 def sources():

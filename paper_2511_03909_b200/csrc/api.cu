@@ -63,7 +63,7 @@ bool sweep2d_supported(int ndim, const int64_t* dims, int T);
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
                            const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                            int num_sms, int freud);
-size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud);
+size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud, int64_t B, int num_sms);
 wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndim, const int64_t* dims,
                              const float* dirs, int d_begin, int Dc, int T, const GridParams* gp, int16_t* cwo,
                              unsigned long long* diff, cudaStream_t st, int num_sms);
@@ -327,7 +327,7 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
     }
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
   } else if (sweep) {
-    void* scr = ar.alloc(sweep2d_scratch_bytes((int)nv, Dc, grid->T, freud ? 1 : 0));
+    void* scr = ar.alloc(sweep2d_scratch_bytes((int)nv, Dc, grid->T, freud ? 1 : 0, B, nsm));
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
     s = launch_sweep2d(dimg, B, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, scr, ov.dev, odtype, st,
                        nsm, freud ? 1 : 0);

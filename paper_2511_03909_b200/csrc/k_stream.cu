@@ -52,10 +52,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
       : "memory");
 }
-// L2 prefetch of [p, p + bytes) (16-byte multiples) through the bulk-copy engine
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // a pointer the compiler cannot re-associate with the 32-bit offsets added to it
 __device__ __forceinline__ const float* opaque(const float* p) {

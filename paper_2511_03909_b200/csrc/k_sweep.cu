@@ -48,17 +48,20 @@ __host__ __device__ constexpr int chunk_bins(int osz) { return kStageRow / osz; 
 // 32-byte records per direction: one per bin at least, + one per 15 vertices, + the prefetch pad
 __host__ __device__ constexpr int sweep_rec_stride(int HW, int Tp) { return Tp + (HW + kRecRows - 1) / kRecRows + 8; }
 // smem of k_sweep2d: cw table [HW][128 B] (1024-aligned) | output stages [32][2 KB] |
-// record rings [32][1 KB] | ring mbarriers [32][2] | image totals [32 words][2].  The
-// staged pixels [HW][68 B] overlay the stages: they are only read by the cw build, before
-// any sweep of the phase uses its stage (the rings stay free, so every warp starts loading
-// its program while the CTA stages pixels and builds cw).
+// record rings [32][1 KB] | ring mbarriers [32][2] | image totals [32 words][2] | pixel
+// mbarrier.  The staged pixels [HW][68 B] overlay the stages: they are only read by the cw
+// build, before any sweep of the phase uses its stage (the rings stay free, so every warp
+// starts loading its program while the CTA stages pixels and builds cw).  The first phase
+// of an image group transposes the pixels from the images and parks the staged block in
+// global scratch (one bulk store, L2-resident); later phases reload it with one bulk copy.
 __host__ __device__ constexpr size_t sweep_cw_bytes(int HW) { return align_up((size_t)HW * 128, 1024); }
 __host__ __device__ constexpr size_t sweep_fixed_bytes() {
-  return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16) + 256;
+  return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16) + 256 + 16;
 }
 __host__ __device__ constexpr size_t sweep_smem_bytes(int HW) {
   return 1024 + sweep_cw_bytes(HW) + sweep_fixed_bytes();
 }
+__host__ __device__ constexpr size_t sweep_pix_bytes(int HW) { return align_up((size_t)HW * kPixStride, 16); }
 __host__ __device__ constexpr bool sweep_pix_fits(int HW) {
   return (size_t)HW * kPixStride <= (size_t)kSweepWarps * kStageBytes;
 }
@@ -324,12 +327,16 @@ __device__ __forceinline__ void sweep_half(uint32_t lane_s, const uint4* __restr
     ring_fill(R, 0, prog, 0, nrec);
     ring_fill(R, 1, prog, 16, nrec);
   }
-  const uint32_t ring_s = smem_u32(R.buf);
+  uint32_t ring_s;  // pinned, see st_s
+  asm volatile("mov.b32 %0, %1;" : "=r"(ring_s) : "r"(smem_u32(R.buf)));
   uint32_t ro = 0;   // byte offset of the next record in the ring (32 records of 32 B)
   int fill = 32;     // first record of the next refill
   int used = 0;      // records consumed
   int B0 = 0, B1 = 0;
-  const uint32_t st_s = smem_u32(st);
+  // pinned (asm): otherwise the compiler re-derives the stage address from the dynamic
+  // shared window (~16 uniform instructions) at every chunk store
+  uint32_t st_s;
+  asm volatile("mov.b32 %0, %1;" : "=r"(st_s) : "r"(smem_u32(st)));
   mbar_wait(R.bar, R.ph & 1u);  // the first half
   R.ph ^= 1u;
   // the rows of one bin: all its records, folded onto (B0, B1)
@@ -432,7 +439,8 @@ template <typename OutT, bool FREUD, bool TMA>
 __global__ void __launch_bounds__(kSweepWarps * 32, 1)
     k_sweep2d(const uint8_t* __restrict__ img, int64_t B, int H, int W, const uint4* __restrict__ recs, int rec_stride,
               const int* __restrict__ qlist, const int* __restrict__ qcount, const int4* __restrict__ split, int Dc,
-              int T, int Tp, OutT* __restrict__ out, const __grid_constant__ CUtensorMap tmap) {
+              int T, int Tp, OutT* __restrict__ out, uint8_t* __restrict__ pix_park,
+              const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1024-aligned (the swizzle pattern of the TMA stores), kept in the shared window
   unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
@@ -443,12 +451,18 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   uint64_t* bars = (uint64_t*)(rings + kSweepWarps * kRingBytes);
   int* totals = (int*)(bars + 2 * kSweepWarps);  // [32 lanes][2]: chi of images (lane, lane + 32)
   uint8_t* pix = stages;  // [HW][kPixStride] u8, overlays the stages: byte 2j + h = image j + 32 h
+  uint64_t* pbar = (uint64_t*)(totals + 2 * 32);  // pixel reload barrier
+  // parked pixels (one staged block per image group) unless CTAs share groups (gridDim.y > 1)
+  const bool park = pix_park != nullptr && gridDim.y == 1;
+  const unsigned pbytes = (unsigned)sweep_pix_bytes(HW);
+  uint32_t pph = 0;
   const int lane = threadIdx.x & 31;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int half = warp & 1, wpair = warp >> 1;
   uint8_t* st = stages + warp * kStageBytes;
   Ring ring{rings + warp * kRingBytes, bars + 2 * warp, 0u};
   if (threadIdx.x < 2 * kSweepWarps) mbar_init(bars + threadIdx.x, 1);
+  if (threadIdx.x == 0) mbar_init(pbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const uint32_t lane_s = (uint32_t)__cvta_generic_to_shared(cwb) + 4u * lane;
@@ -462,7 +476,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t img0 = grp * kSweepImgs;
     const int nimg = (int)((B - img0) < kSweepImgs ? (B - img0) : kSweepImgs);
-    bool need_tot = true;
+    bool need_tot = true, staged = false;
+    uint8_t* parked = park ? pix_park + grp * (int64_t)pbytes : nullptr;
 #pragma unroll 1
     for (int o = 0; o < NPH; ++o) {
       const int qco = qcount[o];
@@ -484,9 +499,20 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
           ring_fill(ring, 1, prog0, 16, nrec0);
         }
       }
+      // the previous phase's generic stage accesses are ordered before the bulk copy below
+      if (park && staged) fence_proxy_async();
       __syncthreads();  // previous phase's sweeps are done with cwb and the stages
-      // stage the group's pixels transposed: image i -> byte 2 (i % 32) + i / 32 of pix[v]
-      if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
+      const bool reload = park && staged;
+      if (reload) {
+        // this group's transposed pixels, parked by its first phase (L2-resident)
+        if (threadIdx.x == 0) {
+          mbar_arrive_expect_tx(pbar, pbytes);
+          bulk_g2s_plain(pix, parked, pbytes, pbar);
+        }
+        mbar_wait(pbar, pph);
+        pph ^= 1u;
+      } else if ((HW & 15) == 0 && ((uintptr_t)img & 15) == 0) {
+        // stage the group's pixels transposed: image i -> byte 2 (i % 32) + i / 32 of pix[v]
         const int per = HW >> 4;
         for (int f = threadIdx.x; f < kSweepImgs * per; f += blockDim.x) {
           const int i = f & (kSweepImgs - 1), v = (f >> 6) << 4;
@@ -503,7 +529,11 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
           pix[v * kPixStride + 2 * (i & 31) + (i >> 5)] = i < nimg ? img[(img0 + i) * HW + v] : (uint8_t)0;
         }
       }
+      const bool park_now = park && !staged;
+      staged = true;
+      if (park_now) fence_proxy_async();  // the STS above, before the bulk store reads them
       __syncthreads();
+      if (park_now && threadIdx.x == 0) bulk_s2g(parked, pix, pbytes);
       if (FREUD) {
         int v = warp;
         int r = v / W, c = v - r * W;
@@ -551,6 +581,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
           }
         }
       }
+      if (park_now && threadIdx.x == 0) tma_wait_read_all();  // pix (= the stages) is read out
       __syncthreads();
       // totals: every cell is counted once in the cw table of ANY phase, so the sum of all cw
       // rows is the image's weighted Euler characteristic (the top bin of every direction):
@@ -662,10 +693,13 @@ bool sweep2d_supported(int ndim, const int64_t* dims, int T) {
 
 static int padded_bins(int T) { return (T + 7) & ~7; }  // a whole number of chunks for int32 and int64
 
-size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud) {
+// parked pixel blocks: only when every CTA owns whole image groups (B >= 64 * SMs-ish)
+static bool sweep_parks(int64_t B, int num_sms) { return (B + kSweepImgs - 1) / kSweepImgs >= num_sms; }
+
+size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud, int64_t B, int num_sms) {
   return (size_t)Dc * sweep_rec_stride(HW, padded_bins(T)) * 32 + 64 + (size_t)(8 + 8 * Dc + 1) * 4 + 64 +
-         (size_t)Dc * 16 + 16 +
-         (freud ? (size_t)5 * HW * Dc * sizeof(int4) + 16 : 0);
+         (size_t)Dc * 16 + 16 + (freud ? (size_t)5 * HW * Dc * sizeof(int4) + 16 : 0) +
+         (sweep_parks(B, num_sms) ? (size_t)((B + kSweepImgs - 1) / kSweepImgs) * sweep_pix_bytes(HW) + 16 : 0);
 }
 
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc,
@@ -682,6 +716,8 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   int* ncorr = (int*)(split + Dc);
   int4* corr = (int4*)align_up((uintptr_t)(ncorr + 1), 16);
   const int corr_cap = freud ? 5 * HW * Dc : 0;
+  uint8_t* pix_park = sweep_parks(B, num_sms) ? (uint8_t*)align_up((uintptr_t)(corr + corr_cap), 16) : nullptr;
+  if (getenv("WECT_SWEEP_NOPARK")) pix_park = nullptr;
   WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 8 * sizeof(int), st));
   WECT_CUDA_TRY(cudaMemsetAsync(ncorr, 0, sizeof(int), st));
   const size_t sort_smem = (size_t)3 * Tp * sizeof(int) + align_up((size_t)HW * 2, 16);
@@ -708,7 +744,7 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
   do {                                                                                                              \
     WECT_CUDA_TRY(cudaFuncSetAttribute(k_sweep2d<OT, FR, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     k_sweep2d<OT, FR, TM><<<grid, kSweepWarps * 32, smem, st>>>(img, B, H, W, recs, rstride, qlist, qcount, split, Dc, T, \
-                                                                 Tp, (OT*)out, tmap);                                   \
+                                                                 Tp, (OT*)out, pix_park, tmap);                         \
     count_launch();                                                                                                 \
   } while (0)
 #define WECT_SWEEP_T(OT, FR) \
