@@ -383,33 +383,38 @@ __device__ __forceinline__ void sweep_half(uint32_t lane_s, const uint4* __restr
 #pragma unroll 1
   for (int ci = 0; ci < nchunk; ++ci) {
     const int q0 = DOWN ? q_hi - (ci + 1) * CB : q_lo + ci * CB;
-    int o0[CB], o1[CB];
-    if (!DOWN) {
+    // one 16-byte half-row (PER bins) at a time: take its bins, store them -- only 2 PER
+    // outputs live in registers; the stage is free once the previous store has read it
 #pragma unroll
-      for (int k = 0; k < CB; ++k) {
-        take_bin();
-        o0[k] = B0;
-        o1[k] = B1;
-      }
-    } else {
+    for (int jj = 0; jj < CB / PER; ++jj) {
+      const int j = DOWN ? CB / PER - 1 - jj : jj;
+      int o0[PER], o1[PER];
+      if (!DOWN) {
 #pragma unroll
-      for (int k = CB - 1; k >= 0; --k) {
-        o0[k] = t0 - B0;  // rows of the bins above k only
-        o1[k] = t1 - B1;
-        take_bin();
-      }
-    }
-    // the previous chunk's TMA store has finished reading the stage
-    if (TMA && lane == 0) tma_wait_read_all();
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < CB / PER; ++j) {
-      if (sizeof(OutT) == 4) {
-        *(int4*)(st + stage_off(lane, j)) = make_int4(o0[4 * j], o0[4 * j + 1], o0[4 * j + 2], o0[4 * j + 3]);
-        *(int4*)(st + stage_off(lane + 32, j)) = make_int4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
+        for (int k = 0; k < PER; ++k) {
+          take_bin();
+          o0[k] = B0;
+          o1[k] = B1;
+        }
       } else {
-        *(longlong2*)(st + stage_off(lane, j)) = make_longlong2(o0[2 * j], o0[2 * j + 1]);
-        *(longlong2*)(st + stage_off(lane + 32, j)) = make_longlong2(o1[2 * j], o1[2 * j + 1]);
+#pragma unroll
+        for (int k = PER - 1; k >= 0; --k) {
+          o0[k] = t0 - B0;  // rows of the bins above k only
+          o1[k] = t1 - B1;
+          take_bin();
+        }
+      }
+      if (jj == 0) {
+        // the previous chunk's TMA store has finished reading the stage
+        if (TMA && lane == 0) tma_wait_read_all();
+        __syncwarp();
+      }
+      if (sizeof(OutT) == 4) {
+        *(int4*)(st + stage_off(lane, j)) = make_int4(o0[0], o0[1 % PER], o0[2 % PER], o0[3 % PER]);
+        *(int4*)(st + stage_off(lane + 32, j)) = make_int4(o1[0], o1[1 % PER], o1[2 % PER], o1[3 % PER]);
+      } else {
+        *(longlong2*)(st + stage_off(lane, j)) = make_longlong2(o0[0], o0[1 % PER]);
+        *(longlong2*)(st + stage_off(lane + 32, j)) = make_longlong2(o1[0], o1[1 % PER]);
       }
     }
     if (TMA) {
