@@ -32,7 +32,7 @@
 
 namespace wect {
 
-constexpr int kRecRows = 15;     // vertex rows per 32-byte record (u16 header + 15 u16 rows)
+constexpr int kRecRows = 14;     // vertex rows per 32-byte record (u16 header + 14 u16 rows + 1 spare)
 constexpr int kSweepWarps = 32;   // two per direction: the bins below / above its split
 constexpr int kSweepImgs = 64;   // images per CTA group: lane l owns images l, l + 32
 constexpr int kPixStride = 68;   // bytes per staged pixel row (17 words: conflict-free transpose)
@@ -54,7 +54,8 @@ __host__ __device__ constexpr int sweep_rec_stride(int HW, int Tp) { return Tp +
 // starts loading its program while the CTA stages pixels and builds cw).  The first phase
 // of an image group transposes the pixels from the images and parks the staged block in
 // global scratch (one bulk store, L2-resident); later phases reload it with one bulk copy.
-__host__ __device__ constexpr size_t sweep_cw_bytes(int HW) { return align_up((size_t)HW * 128, 1024); }
+// (row HW is all zeros: the pad row of odd-sized records)
+__host__ __device__ constexpr size_t sweep_cw_bytes(int HW) { return align_up((size_t)(HW + 1) * 128, 1024); }
 __host__ __device__ constexpr size_t sweep_fixed_bytes() {
   return (size_t)kSweepWarps * (kStageBytes + kRingBytes + 16) + 256 + 16;
 }
@@ -84,13 +85,14 @@ __host__ __device__ __forceinline__ int freud_mask(int t) {
   return m[t];
 }
 
-// Binary-block record layout: a record's n rows occupy, for each set bit of n from the
-// top, a block of 8 / 4 / 2 / 1 slots at slots 0-7 / 8-11 / 12-13 / 14, so the sweep sums
-// them as up to four straight-line blocks of independent gathers (no per-row test).
+// Binary-block record layout: a record's n rows (n even: an odd record is padded with the
+// all-zero row HW) occupy, for each set bit of n from the top, a block of 8 / 4 / 2 slots at
+// slots 0-7 / 8-11 / 12-13, so the sweep sums them as up to three straight-line blocks of
+// independent gathers (no per-row test).
 __host__ __device__ __forceinline__ int rec_slot(int n, int p) {
   int base = 0;
 #pragma unroll
-  for (int blk = 8; blk >= 1; blk >>= 1) {
+  for (int blk = 8; blk >= 2; blk >>= 1) {
     if (n & blk) {
       if (p < blk) return base + p;
       p -= blk;
@@ -202,7 +204,10 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
     const int nrec = c > kRecRows ? (c + kRecRows - 1) / kRecRows : 1;
     for (int j = 0; j < nrec; ++j) {
       const int n = c - j * kRecRows < kRecRows ? c - j * kRecRows : kRecRows;
-      ((uint16_t*)(rec + 2 * (rbase[q] + j)))[0] = (uint16_t)(n | (j + 1 < nrec ? 16 : 0));
+      const int ne = n + (n & 1);
+      uint16_t* r16 = (uint16_t*)(rec + 2 * (rbase[q] + j));
+      r16[0] = (uint16_t)(ne | (j + 1 < nrec ? 16 : 0));
+      if (n & 1) r16[1 + rec_slot(ne, n)] = (uint16_t)HW;  // the zero row
     }
   }
   if (freud) {
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
     const int r = atomicAdd(&counts[bq], -1) - 1;  // position within the bin
     const int j = r / kRecRows, p = r - j * kRecRows;
     const int n = counts_total_rows(bq, j);
-    ((uint16_t*)(rec + 2 * (rbase[bq] + j)))[1 + rec_slot(n, p)] = (uint16_t)v;
+    ((uint16_t*)(rec + 2 * (rbase[bq] + j)))[1 + rec_slot(n + (n & 1), p)] = (uint16_t)v;
   }
 }
 
@@ -372,8 +377,7 @@ __device__ __forceinline__ void sweep_half(uint32_t lane_s, const uint4* __restr
         S += lds32(row_hi(lane_s, b.x)) + lds32(row_lo(lane_s, b.y)) + lds32(row_hi(lane_s, b.y)) +
              lds32(row_lo(lane_s, b.z));
       if (n & 2u) S += lds32(row_hi(lane_s, b.z)) + lds32(row_lo(lane_s, b.w));
-      if (n & 1u) S += lds32(row_hi(lane_s, b.w));
-      // signed packed pair S = s0 + s1 2^16 (mod 2^32), |s0|, |s1| <= 15 * 765
+      // signed packed pair S = s0 + s1 2^16 (mod 2^32), |s0|, |s1| <= 14 * 765
       const int s0 = (int)(int16_t)(S & 0xFFFFu);
       B0 += s0;
       B1 += ((int)S - s0) >> 16;
@@ -467,6 +471,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, 1)
   uint8_t* st = stages + warp * kStageBytes;
   Ring ring{rings + warp * kRingBytes, bars + 2 * warp, 0u};
   if (threadIdx.x < 2 * kSweepWarps) mbar_init(bars + threadIdx.x, 1);
+  if (threadIdx.x < 32) cwb[HW * 32 + threadIdx.x] = 0u;  // the pad row
   if (threadIdx.x == 0) mbar_init(pbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
