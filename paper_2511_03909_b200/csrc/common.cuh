@@ -23,7 +23,7 @@ struct GridParams {
   int32_t T;
   int32_t degenerate;  // hi <= lo (M = 0): every value is bin 0 (reading A6)
   int32_t fp32_only;   // WECT_FP32_ONLY
-  int32_t pad;
+  int32_t covers;      // grids: [lo, hi] holds every height (fast bins need no clamp); else 0
 };
 
 // Segments of the virtual cell index space of an explicit complex: segment 0 is the

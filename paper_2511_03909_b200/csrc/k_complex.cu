@@ -130,7 +130,7 @@ __global__ void k_params_complex(int mode, int n, const unsigned long long* __re
   g.A = (float)A;
   g.B = (float)Bc;
   g.tau = (float)(2.0 * (double)kEps32 * (A * (nn + 2) * R + 2.0 * fabs(Bc) + T + 1.0));
-  g.pad = 0;
+  g.covers = 0;
   *out = g;
 }
 

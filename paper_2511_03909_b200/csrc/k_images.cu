@@ -84,7 +84,9 @@ __global__ void k_grid_params(int ndim, int64_t d0, int64_t d1, int64_t d2, cons
     g.A = (float)A;
     g.B = (float)Bc;
     g.tau = (float)(2.0 * (double)kEps32 * (A * (ndim + 2) * R + 2.0 * fabs(Bc) + T + 1.0));
-    g.pad = 0;
+    // the grid [lo, hi] holds every height of every direction (always for the paper grid):
+    // the fast bin of a voxel far from a bin edge is then in [0, T-1] without clamping
+    g.covers = (!g.fp32_only && !g.degenerate && g.lo <= -red[0] && g.hi >= red[0] && T < (1 << 22)) ? 1 : 0;
     *out = g;
   }
 }
@@ -168,8 +170,8 @@ __global__ void __launch_bounds__(256) k_grid_cw(const uint8_t* __restrict__ img
 // u lies within tau of an integer recompute h exactly in binary64 from the axis tables.
 // The row's orthant weights are staged in smem with coalesced 16-byte loads; the
 // histogram is lane-interleaved [T][32] so atomics never bank-conflict.
-constexpr int kSegVox = 256;     // voxels per staged row segment
-constexpr int kSegStride = 264;  // int16 per staged octant row (132 words = 4 mod 32: conflict-free)
+constexpr int kSegVox = 128;     // voxels per staged row segment
+constexpr int kSegStride = 136;  // int16 per staged octant row (68 words = 4 mod 32: conflict-free)
 
 __device__ __noinline__ int grid_repair(float cx, float cy, float cz, float s0, float s1, float s2, int nd,
                                         const GridParams* gp) {
@@ -222,8 +224,11 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
   const float c0 = (float)((double)(L[0] - 1) / 2.0);
   const int Tm1 = T - 1;
   const uint32_t hlane = (uint32_t)__cvta_generic_to_shared(hist) + 4u * lane;
+  constexpr float kMagic = 12582912.0f;  // 1.5 2^23
+  const bool covers = g.covers != 0;
+  const uint32_t hfast = hlane - 128u * (uint32_t)__float_as_int(kMagic);  // + 128 t = hlane + 128 bin
   const uint32_t* segw = (const uint32_t*)(seg + o * kSegStride);  // this lane's octant row, 2 voxels per word
-  const uint32_t amask = active ? 0xFFFFFFFFu : 0u;  // inactive lanes add nothing
+  // inactive lanes (dl >= Dc) bin direction d_begin into their own column, which the flush drops
   const int64_t nrows = (int64_t)L[1] * L[2];
   const int64_t nv = nrows * L[0];
   const int64_t b = blockIdx.z;
@@ -260,32 +265,76 @@ __global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ c
         seg[oo * kSegStride + nx + (t - oo * (nx8 - nx))] = 0;
       }
       __syncwarp();
-      // 8 voxels per step: one 16-byte load of this lane's octant row, eight fp32 bins
-      // (branch-free clamp), one guard test for the group, eight red.shared adds
-      for (int xi = 0; xi < nx; xi += 8) {
-        const uint4 q = *(const uint4*)(segw + (xi >> 1));
-        const uint32_t wd[4] = {q.x & amask, q.y & amask, q.z & amask, q.w & amask};
-        const float xf = (float)(x0 + xi);
-        int bin[8];
-        float dist[8], dmin = 2.f;
+      // 8 voxels per step: one 16-byte load of this lane's octant row, eight fp32 bins, one
+      // guard test for the group, eight red.shared adds
+      if (covers) {
+        // ceil without the conversion unit: t = u + 1.5 2^23 rounded up is 1.5 2^23 + ceil(u)
+        // (|u| < 2^22), so t's bit pattern minus the constant's is the bin; e = ceil(u) - u
+        // (exact) in [0, 1) is the distance to the bin edges: near an edge iff e < tau or
+        // e > 1 - tau.  No clamp: a bin taken here is ceil(u64) in [0, T-1] (A1).
+        for (int xi = 0; xi < nx; xi += 8) {
+          const uint4 q = *(const uint4*)(segw + (xi >> 1));
+          const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+          const float xf = (float)(x0 + xi);
+          uint32_t adr[8];
+          float emin = 1.f, emax = 0.f;
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const float u = fmaf(xf + (float)h, a0, U0);  // x0 + xi + h is exact in fp32
-          bin[h] = max(0, min(__float2int_ru(u), Tm1));
-          dist[h] = fabsf(u - rintf(u));
-          dmin = fminf(dmin, dist[h]);
+          for (int h = 0; h < 8; ++h) {
+            const float u = fmaf(xf + (float)h, a0, U0);  // x0 + xi + h is exact in fp32
+            const float t = __fadd_ru(u, kMagic);
+            const float e = (t - kMagic) - u;
+            emin = fminf(emin, e);
+            emax = fmaxf(emax, e);
+            adr[h] = hfast + 128u * (uint32_t)__float_as_int(t);
+          }
+          const int nvalid = nx - xi;
+          if (nvalid < 8) {  // the row's zero-weight padding voxels: any in-range bin (u may be far outside)
+#pragma unroll
+            for (int h = 1; h < 8; ++h)
+              if (h >= nvalid) adr[h] = hlane;
+          }
+          // warp vote: a uniform branch, no reconvergence barrier in the common case
+          if (__builtin_expect(__any_sync(0xffffffffu, emin < tau || emax > 1.f - tau), 0)) {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+              const float u = fmaf(xf + (float)h, a0, U0);
+              const float e = (__fadd_ru(u, kMagic) - kMagic) - u;
+              if ((e < tau || e > 1.f - tau) && h < nvalid)  // padding voxels need no repair
+                adr[h] = hlane + 128u * (uint32_t)grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const int w = (h & 1) ? (int)wd[h >> 1] >> 16 : (int)(int16_t)(wd[h >> 1] & 0xFFFFu);
+            red_shared_add(adr[h], w);
+          }
         }
-        if (__builtin_expect(dmin < tau, 0)) {  // some voxel of the group sits near a bin edge
-          const int nvalid = nx - xi;  // padding voxels need no repair
+      } else {
+        for (int xi = 0; xi < nx; xi += 8) {
+          const uint4 q = *(const uint4*)(segw + (xi >> 1));
+          const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+          const float xf = (float)(x0 + xi);
+          int bin[8];
+          float dist[8], dmin = 2.f;
 #pragma unroll
-          for (int h = 0; h < 8; ++h)
-            if (dist[h] < tau && h < nvalid)
-              bin[h] = grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
-        }
+          for (int h = 0; h < 8; ++h) {
+            const float u = fmaf(xf + (float)h, a0, U0);  // x0 + xi + h is exact in fp32
+            bin[h] = max(0, min(__float2int_ru(u), Tm1));
+            dist[h] = fabsf(u - rintf(u));
+            dmin = fminf(dmin, dist[h]);
+          }
+          if (__builtin_expect(dmin < tau, 0)) {  // some voxel of the group sits near a bin edge
+            const int nvalid = nx - xi;  // padding voxels need no repair
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const int w = (h & 1) ? (int)wd[h >> 1] >> 16 : (int)(int16_t)(wd[h >> 1] & 0xFFFFu);
-          red_shared_add(hlane + 128u * (uint32_t)bin[h], w);
+            for (int h = 0; h < 8; ++h)
+              if (dist[h] < tau && h < nvalid)
+                bin[h] = grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
+          }
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const int w = (h & 1) ? (int)wd[h >> 1] >> 16 : (int)(int16_t)(wd[h >> 1] & 0xFFFFu);
+            red_shared_add(hlane + 128u * (uint32_t)bin[h], w);
+          }
         }
       }
       __syncwarp();

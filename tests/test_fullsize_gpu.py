@@ -172,6 +172,25 @@ def test_ties_volume_histogram_path(T):
     assert (g == oracle.wect_images(img, dirs, T, maxheight_override=0.5)).all()
 
 
+@pytest.mark.parametrize("T", [33, 65, 129, 257])
+def test_ties_volume_covering_grid_fast_bins(T):
+    """17^3 volume, axis directions only, the paper grid (M computed = 1/2, so [-M, M] holds
+    every height and k_grid_hist takes its clamp-free rounded-up-add bins): with T - 1 a
+    multiple of 16 every vertex height is exactly a bin edge -- repairs fire, bit-exact."""
+    img = np.random.default_rng(T + 1).integers(0, 256, (2, 17, 17, 17), dtype=np.uint8)
+    dirs = _tie_dirs(3, 0, T)[:6]
+    w.repair_count(reset=True)
+    g = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs).to(DEV), T,
+                      out_dtype="int64").cpu().numpy()
+    assert w.repair_count() > 0
+    assert (g == oracle.wect_images(img, dirs, T)).all()
+    # and with random directions added (M then from the grid corners, no ties)
+    dirs2 = np.concatenate([dirs, synth.directions_sphere(40, 3, T)]).astype(np.float32)
+    g2 = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs2).to(DEV), T,
+                       out_dtype="int32").cpu().numpy()
+    assert (g2 == oracle.wect_images(img, dirs2, T)).all()
+
+
 def test_ties_large_image_histogram_path():
     """A 2-D image too large for the sweep (40 x 33) takes k_grid_hist: axis / 45-degree
     directions with T - 1 = 4 (L - 1) on the long axis."""
