@@ -60,6 +60,11 @@ struct TimeScope {
 wect_status launch_grid_params(int ndim, const int64_t* dims, const float* dirs, int D, const wect_grid& grid,
                                GridParams* gp, cudaStream_t st);
 bool sweep2d_supported(int ndim, const int64_t* dims, int T);
+bool mma2d_supported(int ndim, const int64_t* dims, int T);
+size_t mma2d_scratch_bytes(int HW, int Dc, int T);
+wect_status launch_mma2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
+                         const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
+                         int num_sms);
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
                            const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                            int num_sms, int freud);
@@ -300,6 +305,9 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   const bool sweep = sweep2d_supported(ndim, dims, grid->T) && !(freud && getenv("WECT_FREUD_HIST"));
   if (!sweep && grid->T > 1024) return fail(WECT_ENOTSUP, "T > 1024 needs the sweep path (2D cubical, H*W <= 1024)");
   if (B == 0 || Dc == 0) return WECT_OK;
+  // the tensor-core contraction (k_mma.cu, cubical 2-D): WECT_IMAGES_MMA=1 selects it
+  const char* mma_env = getenv("WECT_IMAGES_MMA");
+  const bool mma = !freud && mma_env && mma_env[0] == '1' && mma2d_supported(ndim, dims, grid->T);
 
   const int nsm = num_sms_current();
   Arena ar(st);
@@ -326,6 +334,10 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
       s = launch_freud(dimg, b0, nb, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, w6, diff, st, nsm);
     }
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
+  } else if (mma) {
+    void* scr = ar.alloc(mma2d_scratch_bytes((int)nv, Dc, grid->T));
+    if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
+    s = launch_mma2d(dimg, B, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, scr, ov.dev, odtype, st, nsm);
   } else if (sweep) {
     void* scr = ar.alloc(sweep2d_scratch_bytes((int)nv, Dc, grid->T, freud ? 1 : 0, B, nsm));
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
