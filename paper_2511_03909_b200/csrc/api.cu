@@ -69,8 +69,9 @@ wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const fl
                            const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                            int num_sms, int freud);
 size_t sweep2d_scratch_bytes(int HW, int Dc, int T, int freud, int64_t B, int num_sms);
+bool grid_hist_fused(int ndim, const int64_t* dims, const uint8_t* img);
 wect_status launch_grid_hist(const uint8_t* img, int64_t b0, int64_t nb, int ndim, const int64_t* dims,
-                             const float* dirs, int d_begin, int Dc, int T, const GridParams* gp, int16_t* cwo,
+                             const float* dirs, int d_begin, int Dc, int T, const GridParams* gp, int16_t* cwo, int* perm,
                              unsigned long long* diff, cudaStream_t st, int num_sms);
 wect_status launch_vmax(int n, const float* coords, int64_t k0, const float* dirs, int D, float* vmax,
                         unsigned int* m32, unsigned int* r1, unsigned int* smax, unsigned long long* m64,
@@ -346,18 +347,20 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   } else {
     const size_t nbins = (size_t)B * Dc * grid->T;
     unsigned long long* diff = (unsigned long long*)ar.alloc(nbins * 8);
-    // orthant weights for a chunk of images: at most ~1 GiB of scratch
+    // orthant weights for a chunk of images: at most ~1 GiB of scratch (none when fused)
+    const bool fused = grid_hist_fused(ndim, dims, dimg);
     const int64_t per_img = nv * (1 << ndim) * 2;
-    int64_t chunk = ((int64_t)1 << 30) / per_img;
+    int64_t chunk = fused ? B : ((int64_t)1 << 30) / per_img;
     if (chunk < 1) chunk = 1;
     if (chunk > 65535) chunk = 65535;  // k_grid_hist takes the image from gridDim.z
     if (chunk > B) chunk = B;
-    int16_t* cwo = (int16_t*)ar.alloc((size_t)chunk * per_img);
+    int16_t* cwo = fused ? nullptr : (int16_t*)ar.alloc((size_t)chunk * per_img);
+    int* perm = (int*)ar.alloc((size_t)Dc * sizeof(int));
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
     WECT_CUDA_TRY(cudaMemsetAsync(diff, 0, nbins * 8, st));
     for (int64_t b0 = 0; b0 < B && s == WECT_OK; b0 += chunk) {
       int64_t nb = B - b0 < chunk ? B - b0 : chunk;
-      s = launch_grid_hist(dimg, b0, nb, ndim, dims, ddirs, d_begin, Dc, grid->T, gp, cwo, diff, st, nsm);
+      s = launch_grid_hist(dimg, b0, nb, ndim, dims, ddirs, d_begin, Dc, grid->T, gp, cwo, perm, diff, st, nsm);
     }
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
   }

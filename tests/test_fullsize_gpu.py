@@ -243,3 +243,37 @@ def test_ties_lattice_mesh_backward():
     ov, oc = oracle.wect_complex_grad(cx, dirs, T, G, maxheight_override=0.5)
     assert np.array_equal(gv.cpu().numpy(), ov)
     assert all(np.array_equal(a.cpu().numpy(), b) for a, b in zip(gc, oc))
+
+
+@pytest.mark.parametrize("T", [39, 77])
+def test_fused_grid_hist_ties_and_unfused_ab(T, monkeypatch):
+    """WECT_GRID_FUSED=1 on a volume whose x axis is a multiple of 4: the fused k_grid_hist
+    (orthant weights computed from the pixels of each row segment, directions sorted by
+    orthant).  9 x 9 x 20 (x spacing 1/19), axis directions only: M = 1/2 and T - 1 a multiple
+    of 19 put every x-axis vertex height on a bin edge -- repairs fire; then random directions;
+    both bit-exact vs O2, and equal to the default table path (k_grid_cw)."""
+    monkeypatch.setenv("WECT_GRID_FUSED", "1")
+    img = np.random.default_rng(T + 5).integers(0, 256, (3, 9, 9, 20), dtype=np.uint8)
+    dirs = _tie_dirs(3, 0, T)[:6]
+    w.repair_count(reset=True)
+    g = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs).to(DEV), T, out_dtype="int64").cpu().numpy()
+    assert w.repair_count() > 0
+    assert (g == oracle.wect_images(img, dirs, T)).all()
+    dirs2 = np.concatenate([dirs, synth.directions_sphere(70, 3, T)]).astype(np.float32)
+    o2 = oracle.wect_images(img, dirs2, T)
+    g2 = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs2).to(DEV), T, out_dtype="int32").cpu().numpy()
+    assert (g2 == o2).all()
+    monkeypatch.delenv("WECT_GRID_FUSED")
+    g3 = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs2).to(DEV), T, out_dtype="int32").cpu().numpy()
+    assert (g3 == o2).all()
+
+
+def test_fused_grid_hist_2d_large_images(monkeypatch):
+    """2-D images too large for the sweep with a width that is a multiple of 4 (36 x 44): the
+    fused histogram path in 2-D, x-border groups at both ends, ragged last segment."""
+    monkeypatch.setenv("WECT_GRID_FUSED", "1")
+    img = np.random.default_rng(11).integers(0, 256, (5, 36, 44), dtype=np.uint8)
+    dirs = np.concatenate([_tie_dirs(2, 0, 1), synth.directions_s1(41)]).astype(np.float32)
+    for T in (43, 130):
+        g = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs).to(DEV), T, out_dtype="int64").cpu().numpy()
+        assert (g == oracle.wect_images(img, dirs, T)).all()
