@@ -13,6 +13,7 @@
 // direction); a cell costs `arity` coalesced 128-byte row loads (L2-resident for meshes
 // stored in spatial order) and a packed max, independent of n.
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -453,8 +454,13 @@ static wect_status launch_vb_n(bool floatw, const Segs& segs_in, const float* co
   int nstep;
   int ws = 0;
   if (bucket) {
-    while ((k0 >> ws) >= kBucketMax) ++ws;
-    if (ws < 16) ws = 16;  // windows of >= 64K vertices (8 MB of VB rows)
+    // ~8-12 windows per call: per-step overhead falls with fewer steps faster than the
+    // wider window costs in L2 misses (measured on cfg4, 10M vertices: 2^16-vertex windows
+    // 3.33 ms per tile, 2^18 3.20, 2^20 2.68, 2^22 2.85, one window 3.02; cfg5: 2^16 4.46,
+    // 2^18 4.06, 2^20 4.01)
+    ws = 16;
+    while ((k0 >> ws) > 12) ++ws;
+    if (const char* e = getenv("WECT_VB_WS")) ws = atoi(e);  // A/B experiments
     nstep = (int)((k0 - 1) >> ws) + 1;
   } else {
     // every warp gets ~4 batches of EVERY segment per step (balanced, narrow window)
