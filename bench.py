@@ -408,7 +408,9 @@ def run_ours(args, rank, world, local_rank):
     if wl["kind"] == "ecfimg":
         kname, bound = ("k_ecf_img2d_w4", "hbm") if args.config == "ecfimg" else ("k_ecf_img2d_rows", "alu")
     elif wl["kind"] == "images" and (args.config in ("0", "1") or wl.get("freudenthal")):
-        kname, bound = "k_sweep2d", "hbm"
+        # WECT_IMAGES_MMA=1: the opt-in tensor-core contraction (k_mma.cu) instead of the sweep
+        mma = os.environ.get("WECT_IMAGES_MMA") == "1" and not wl.get("freudenthal")
+        kname, bound = ("k_mma2d" if mma else "k_sweep2d"), "hbm"
     elif wl["kind"] == "images":
         kname, bound = "k_grid_hist", "alu"
     elif wl["kind"] == "grad":
