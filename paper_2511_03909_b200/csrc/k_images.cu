@@ -252,7 +252,7 @@ __device__ __forceinline__ uint2 fused_cw4(const uint8_t* __restrict__ im, int x
 }
 
 template <int ND, bool FUSED>
-__global__ void __launch_bounds__(256) k_grid_hist(const int16_t* __restrict__ cwo, const uint8_t* __restrict__ img,
+__global__ void __launch_bounds__(256, 3) k_grid_hist(const int16_t* __restrict__ cwo, const uint8_t* __restrict__ img,
                                                    const int* __restrict__ perm, int64_t d0, int64_t d1, int64_t d2,
                                                    const float* __restrict__ dirs, int d_begin, int Dc,
                                                    const GridParams* __restrict__ gp, int64_t slice_rows,
