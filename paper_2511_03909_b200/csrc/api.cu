@@ -308,7 +308,9 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   if (B == 0 || Dc == 0) return WECT_OK;
   // the tensor-core contraction (k_mma.cu, cubical 2-D): WECT_IMAGES_MMA=1 selects it
   const char* mma_env = getenv("WECT_IMAGES_MMA");
-  const bool mma = !freud && mma_env && mma_env[0] == '1' && mma2d_supported(ndim, dims, grid->T);
+  // (its indicator operand grows with the number of directions: at most 1 GiB of scratch)
+  const bool mma = !freud && mma_env && mma_env[0] == '1' && mma2d_supported(ndim, dims, grid->T) &&
+                   mma2d_scratch_bytes((int)nv, Dc, grid->T) <= ((size_t)1 << 30);
 
   const int nsm = num_sms_current();
   Arena ar(st);

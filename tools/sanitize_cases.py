@@ -64,6 +64,18 @@ def main(case):
         w.sync_status()
         ov, oc = oracle.wect_complex_grad(cx, dirs, 64, G)
         assert np.array_equal(gv.cpu().numpy(), ov) and all(np.array_equal(a.cpu().numpy(), b) for a, b in zip(gc, oc))
+    elif case == "mma":  # k_mma_dirs / k_mma_passes / k_mma_bimg + k_mma2d (tcgen05, TMEM, bulk copies)
+        os.environ["WECT_IMAGES_MMA"] = "1"
+        img = g.integers(0, 256, (200, 28, 28), dtype=np.uint8)
+        dirs = synth.directions_s1(19)
+        got = w.wect_images(T_(img), T_(dirs), 128).cpu().numpy()
+        assert (got == oracle.wect_images(img, dirs, 128)).all()
+    elif case == "grid_fused":  # k_dir_perm + the fused k_grid_hist (orthant weights from the pixels)
+        os.environ["WECT_GRID_FUSED"] = "1"
+        vol = g.integers(0, 256, (2, 9, 10, 12), dtype=np.uint8)
+        dirs = synth.directions_sphere(40, 3, 6)
+        got = w.wect_images(T_(vol), T_(dirs), 32, out_dtype="int64").cpu().numpy()
+        assert (got == oracle.wect_images(vol, dirs, 32)).all()
     else:
         raise SystemExit(f"unknown case {case}")
     torch.cuda.synchronize()
