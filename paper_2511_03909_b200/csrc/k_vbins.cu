@@ -90,7 +90,14 @@ __device__ __forceinline__ void hist_add(int* h, int w) { atomicAdd(h, w); }
 __device__ __forceinline__ void hist_add(float* h, float w) { atomicAdd(h, w); }
 
 constexpr int kVbBatch = 32;  // cells per warp batch
-constexpr int kVbWarps = 32;  // warps per CTA (one CTA per SM: MLP for the row gathers)
+#ifndef WECT_VB_WARPS
+#define WECT_VB_WARPS 32
+#endif
+#ifndef WECT_VB_U
+#define WECT_VB_U 4
+#endif
+constexpr int kVbWarps = WECT_VB_WARPS;  // warps per CTA (one CTA per SM: MLP for the row gathers)
+constexpr int kVbU = WECT_VB_U;          // cells per group: all kVbU x arity row loads in flight
 
 // nb cells of arity AR (0: runtime `arr`) from the warp's staged ids: four cells at a
 // time, all 4*AR row loads issued before the packed max and the atomics.
@@ -128,17 +135,17 @@ template <int AR, bool FLOATW, bool DIRECT, typename Acc>
 __device__ __forceinline__ void vb_batch(const int* rec, int nb, const uint32_t* __restrict__ vbl, uint32_t hsa,
                                          Acc* hl, unsigned long long* drow, int T, bool aa, bool ab) {
   constexpr int RS = rec_stride(AR);
-  for (int j = 0; j < nb; j += 4) {
-    int r[4][RS];
+  for (int j = 0; j < nb; j += kVbU) {
+    int r[kVbU][RS];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) load_rec<RS>(rec + (j + u) * RS, r[u]);  // records past nb are zero
-    uint32_t x[4][AR];
+    for (int u = 0; u < kVbU; ++u) load_rec<RS>(rec + (j + u) * RS, r[u]);  // records past nb are zero
+    uint32_t x[kVbU][AR];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kVbU; ++u)
 #pragma unroll
       for (int t = 0; t < AR; ++t) x[u][t] = __ldg(vbl + (int64_t)r[u][t] * 32);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kVbU; ++u) {
       uint32_t m2 = x[u][0];
 #pragma unroll
       for (int t = 1; t < AR; ++t) m2 = __vmaxu2(m2, x[u][t]);
