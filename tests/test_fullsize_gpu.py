@@ -277,3 +277,16 @@ def test_fused_grid_hist_2d_large_images(monkeypatch):
     for T in (43, 130):
         g = w.wect_images(torch.from_numpy(img).to(DEV), torch.from_numpy(dirs).to(DEV), T, out_dtype="int64").cpu().numpy()
         assert (g == oracle.wect_images(img, dirs, T)).all()
+
+
+@pytest.mark.parametrize("T", [33, 65, 129])
+def test_ties_lattice_mesh_covering_grid(T):
+    """Lattice mesh, axis directions only (repeated to D = 30 > 24: k_vbins + k_cells_vb), the
+    paper grid (M computed = 1/2 from the same vertices and directions): T - 1 a multiple of
+    32 puts every vertex height on a bin edge -- repairs fire, bit-exact vs O2."""
+    cx = _lattice_mesh(33, 33, T + 1)
+    dirs = np.tile(_tie_dirs(3, 0, T)[:6], (5, 1))
+    w.repair_count(reset=True)
+    g = _gpu_complex(cx, dirs, T)
+    assert w.repair_count() > 0
+    assert (g == oracle.wect_complex(cx, dirs, T)).all()
