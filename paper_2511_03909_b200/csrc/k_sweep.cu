@@ -164,20 +164,37 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
     __syncwarp();
     // split bin (a multiple of the 8-bin output chunk): the lower warp sweeps [0, sb) upward,
-    // the upper warp [sb, Tp) downward; balanced on ~3.5 instructions per row + ~22 per record
-    if (lane == 0) {
-      int wtot = 0;
-      for (int q = 0; q < Tp; ++q) wtot += 7 * counts[q] + 44 * (counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1);
-      int sb = 0, acc = 0, best = wtot;
-      for (int c = 0; c <= Tp; c += 8) {
-        const int d = abs(2 * acc - wtot);
-        if (d < best) { best = d; sb = c; }
-        for (int q = c; q < c + 8 && q < Tp; ++q)
-          acc += 7 * counts[q] + 44 * (counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1);
+    // the upper warp [sb, Tp) downward; balanced on ~3.5 instructions per row + ~22 per record.
+    // Warp-parallel: a scan of the per-bin costs, each lane's chunk boundaries scored
+    // |2 acc - total|, and the smallest (score, boundary) taken by one warp min-reduction.
+    {
+      auto cost = [&](int q) { return 7 * counts[q] + 44 * (counts[q] > kRecRows ? (counts[q] + kRecRows - 1) / kRecRows : 1); };
+      int cs = 0;
+      for (int q = q0; q < q0 + per && q < Tp; ++q) cs += cost(q);
+      int cinc = cs;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, cinc, o);
+        if (lane >= o) cinc += t;
       }
+      const int wtot = __shfl_sync(0xffffffffu, cinc, 31);
+      int acc = cinc - cs;
+      unsigned key = lane == 31 ? ((unsigned)wtot << 10) | (unsigned)(Tp >> 3) : 0xFFFFFFFFu;  // boundary Tp
+      for (int q = q0; q < q0 + per && q < Tp; ++q) {
+        if ((q & 7) == 0) {
+          const unsigned k = ((unsigned)abs(2 * acc - wtot) << 10) | (unsigned)(q >> 3);
+          key = k < key ? k : key;
+        }
+        acc += cost(q);
+      }
+      key = __reduce_min_sync(0xffffffffu, key);
+      if (lane == 0) sh_split = (int)(key & 1023u) << 3;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int sb = sh_split;
       const int nl = sb < Tp ? rbase[sb] : tot;
       split[dl] = make_int4(nl, tot - nl, sb, 0);
-      sh_split = sb;
       sh_nl = nl;
       sh_tot = tot;
     }
