@@ -65,6 +65,10 @@ size_t mma2d_scratch_bytes(int HW, int Dc, int T);
 wect_status launch_mma2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
                          const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                          int num_sms);
+bool mma2_usable(void* out, int64_t B, int Dc, int T, wect_dtype odtype);
+size_t mma2_scratch_bytes(int HW, int Dc, int T, int64_t B);
+wect_status launch_mma2(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
+                        const GridParams* gp, void* scratch, void* out, cudaStream_t st, int num_sms);
 wect_status launch_sweep2d(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
                            const GridParams* gp, void* scratch, void* out, wect_dtype odtype, cudaStream_t st,
                            int num_sms, int freud);
@@ -309,8 +313,9 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
   // the tensor-core contraction (k_mma.cu, cubical 2-D): WECT_IMAGES_MMA=1 selects it
   const char* mma_env = getenv("WECT_IMAGES_MMA");
   // (its indicator operand grows with the number of directions: at most 1 GiB of scratch)
-  const bool mma = !freud && mma_env && mma_env[0] == '1' && mma2d_supported(ndim, dims, grid->T) &&
-                   mma2d_scratch_bytes((int)nv, Dc, grid->T) <= ((size_t)1 << 30);
+  const bool mma = !freud && mma_env && (mma_env[0] == '1' || mma_env[0] == '2') &&
+                   mma2d_supported(ndim, dims, grid->T) && mma2d_scratch_bytes((int)nv, Dc, grid->T) <= ((size_t)1 << 30);
+  const bool mma2 = mma && mma_env[0] == '2';
 
   const int nsm = num_sms_current();
   Arena ar(st);
@@ -337,6 +342,13 @@ wect_status wect_images(const uint8_t* img, int64_t B, int32_t ndim, const int64
       s = launch_freud(dimg, b0, nb, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, w6, diff, st, nsm);
     }
     if (s == WECT_OK) s = launch_finalize(diff, false, (int64_t)B * Dc, grid->T, ov.dev, odtype, st);
+  } else if (mma2 && mma2_usable(ov.dev, B, Dc, grid->T, odtype) &&
+             mma2_scratch_bytes((int)nv, Dc, grid->T, B) <= ((size_t)3 << 30)) {
+    // WECT_IMAGES_MMA=2: the second contraction kernel (MN-major A from transposed pixels,
+    // TMA-store epilogue); =1: the first (faster of the two)
+    void* scr = ar.alloc(mma2_scratch_bytes((int)nv, Dc, grid->T, B));
+    if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);
+    s = launch_mma2(dimg, B, (int)dims[0], (int)dims[1], ddirs, d_begin, Dc, grid->T, gp, scr, ov.dev, st, nsm);
   } else if (mma) {
     void* scr = ar.alloc(mma2d_scratch_bytes((int)nv, Dc, grid->T));
     if (ar.err != cudaSuccess) return fail_cuda(ar.err, "scratch", __FILE__, __LINE__);

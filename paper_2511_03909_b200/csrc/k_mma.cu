@@ -28,6 +28,9 @@
 //                TMEM columns 0-255 and 256-511; one thread streams the B chunks in by
 //                cp.async.bulk (3-stage ring); 8 epilogue warps read TMEM (tcgen05.ld),
 //                remove the constant with one fp32 add and store int32 / int64.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -552,6 +555,372 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
   }
 }
 
+// ===========================================================================
+// Version 2 (WECT_IMAGES_MMA=2; v1 above is WECT_IMAGES_MMA=1).  What v1's measurements
+// pointed at: the staged pixels (101 KB of shared memory) left room for 3 shallow stages, and
+// the epilogue's 16-byte-per-image stores were slow.  v2 keeps no pixels in shared memory:
+// a prepass writes each 128-image tile transposed, `pixT[tile][v][128 images]` u8, and the
+// builders read it through L1 (lane = 4 images, one coalesced 128-byte line per vertex), so
+// A is written MN-major (images contiguous: SWIZZLE_128B atoms of 64 images x 8 vertices).
+// K chunks of 64 vertices (A 16 KB, B 32 KB per stage, 4 stages); one pass (N = 256) per
+// accumulator, TMEM double-buffered (2 x 256 columns) so the epilogue of a pass overlaps the
+// next pass's MMAs; 4 epilogue warps stage 32 images x 32 bins (128-byte rows, 128B swizzle)
+// and write them with TMA tensor stores.  Bit-exact, but slower than v1 on cfg2 (3.31 vs
+// 1.55 ms): the transposed-pixel reads miss L1 (the 4 stages leave ~30 KB of it) and stall
+// the builders on L2 latency (58 % long-scoreboard), and streaming B per 128-image tile is
+// 8 KB per M128-N256-K16 MMA, ~62 B/cycle per SM -- at or above the L2 share of an SM, so a
+// contraction form needs 2-CTA (cta_group::2) B sharing / multicast before it can compete.
+// ===========================================================================
+constexpr int kM2K = 64;                                    // vertices per K chunk
+constexpr int kM2Stages = 4;
+constexpr int kM2Build = 8;                                 // builder warps: 8 vertices each
+constexpr int kM2Epi = 4;                                   // epilogue warps: TMEM lanes 32 e ..
+constexpr int kM2MmaWarp = kM2Build + kM2Epi;               // + 1: the B loader
+constexpr int kM2Threads = (kM2MmaWarp + 2) * 32;
+constexpr size_t kM2AStage = (size_t)kMmaM * kM2K * 2;      // 16 KB
+constexpr size_t kM2BStage = (size_t)kMmaNmax * kM2K * 2;   // 32 KB
+constexpr size_t kM2EStage = 32 * 128;                      // 4 KB: 32 images x 128 bytes
+__host__ __device__ constexpr int m2_kc(int HW) { return (HW + kM2K - 1) / kM2K; }
+__host__ __device__ constexpr size_t m2_smem_bytes() {
+  return 1024 + kM2Stages * (kM2AStage + kM2BStage) + (size_t)kM2Epi * 2 * kM2EStage + 256;
+}
+
+// K-major SWIZZLE_128B (B: rows of 64 fp16 = 128 bytes, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t umma_desc_k128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// MN-major SWIZZLE_128B (A: atoms of 64 images (128 B) x 8 vertices; the two image atoms
+// 1024 B apart (LBO), vertex atoms 2048 B apart (SBO))
+__device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(1024 >> 4) << 16) | ((uint64_t)(2048 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// transposed tiles: block (tile, 128-vertex slice); pixT[tile][v][i] = img[tile*128 + i][v]
+__global__ void __launch_bounds__(256) k_mma2_pixt(const uint8_t* __restrict__ img, int64_t B, int HW,
+                                                   uint8_t* __restrict__ pixT) {
+  __shared__ uint8_t sm[128][129];
+  const int64_t tile = blockIdx.x;
+  const int v0 = blockIdx.y * 128;
+  const int nv = HW - v0 < 128 ? HW - v0 : 128;
+  for (int e = threadIdx.x; e < 128 * 128; e += blockDim.x) {
+    const int i = e >> 7, v = e & 127;
+    const int64_t im = tile * 128 + i;
+    sm[i][v] = (im < B && v < nv) ? img[im * HW + v0 + v] : (uint8_t)0;
+  }
+  __syncthreads();
+  uint32_t* dst = (uint32_t*)(pixT + (tile * HW + v0) * 128);
+  for (int e = threadIdx.x; e < nv * 32; e += blockDim.x) {
+    const int v = e >> 5, t = e & 31;
+    dst[e] = (uint32_t)sm[4 * t][v] | ((uint32_t)sm[4 * t + 1][v] << 8) | ((uint32_t)sm[4 * t + 2][v] << 16) |
+             ((uint32_t)sm[4 * t + 3][v] << 24);
+  }
+}
+
+// vertex flags: bit 0 row r + 1 exists, bit 1 row r - 1, bit 2 column c + 1, bit 3 column c - 1
+__global__ void k_mma2_vflags(int H, int W, uint8_t* __restrict__ vf) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < H * W; v += gridDim.x * blockDim.x) {
+    const int r = v / W, c = v - r * W;
+    vf[v] = (uint8_t)((r + 1 < H ? 1 : 0) | (r >= 1 ? 2 : 0) | (c + 1 < W ? 4 : 0) | (c >= 1 ? 8 : 0));
+  }
+}
+
+// B operand of (pass, 64-vertex chunk): K-major SWIZZLE_128B rows n = j Tq + q
+__global__ void __launch_bounds__(256) k_mma2_bimg(int HW, int T, int Tq, int N, int KC, const int* __restrict__ npass,
+                                                   const int* __restrict__ tab, const uint16_t* __restrict__ vbin,
+                                                   const int* __restrict__ cum, uint4* __restrict__ bimg,
+                                                   float* __restrict__ cfix) {
+  const int p = blockIdx.x / KC, kc = blockIdx.x - p * KC;
+  if (p >= *npass) return;
+  const int* t = tab + p * kMmaPassCols;
+  const int nd = t[1];
+  uint4* im = bimg + ((int64_t)p * KC + kc) * (N * kM2K * 2 / 16);
+  for (int e = threadIdx.x; e < N * 8; e += blockDim.x) {
+    const int n = e >> 3, c = e & 7;
+    const int j = n / Tq, q = n - j * Tq;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    if (j < nd && q < T) {
+      const uint16_t* vb = vbin + (int64_t)t[2 + j] * HW;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int v = kc * kM2K + c * 8 + k;
+        if (v < HW && (int)vb[v] <= q) w[k >> 1] |= 0x3C00u << (16 * (k & 1));
+      }
+    }
+    im[n * 8 + (c ^ (n & 7))] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (kc == 0)
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const int j = n / Tq, q = n - j * Tq;
+      cfix[(int64_t)p * N + n] =
+          (j < nd && q < T) ? kMmaMagic - 1536.f * (float)cum[(int64_t)t[2 + j] * T + q] : kMmaMagic;
+    }
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kM2Threads, 1)
+    k_mma2(const uint8_t* __restrict__ pixT, const uint8_t* __restrict__ vflags, int64_t B, int H, int W, int T,
+           int Tq, int N, int KC, const int* __restrict__ info, const int* __restrict__ tab,
+           const uint4* __restrict__ bimg, const float* __restrict__ cfix, const __grid_constant__ CUtensorMap omap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  const int HW = H * W;
+  uint8_t* As = smem;                                     // [S][16 KB] MN-major
+  uint8_t* Bs = As + kM2Stages * kM2AStage;               // [S][32 KB] K-major
+  uint8_t* Es = Bs + kM2Stages * kM2BStage;               // [4 warps][2][4 KB] epilogue stages
+  uint64_t* bars = (uint64_t*)(Es + kM2Epi * 2 * kM2EStage);
+  uint64_t* afull = bars;                 // [S]
+  uint64_t* bfull = bars + kM2Stages;     // [S]
+  uint64_t* sdone = bars + 2 * kM2Stages; // [S]
+  uint64_t* tfull = bars + 3 * kM2Stages; // [2]
+  uint64_t* tempty = tfull + 2;           // [2]
+  uint32_t* tmem_hold = (uint32_t*)(tempty + 2);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int64_t ntiles = (B + kMmaM - 1) / kMmaM, nunits = ntiles * 4;
+  const unsigned bbytes = (unsigned)(N * kM2K * 2);
+  __shared__ int qf[4], qn[4];
+  if (tid < 4) {
+    qf[tid] = info[1 + tid];
+    qn[tid] = info[5 + tid];
+  }
+  __syncthreads();
+  const int64_t u_begin = nunits * blockIdx.x / gridDim.x, u_end = nunits * (blockIdx.x + 1) / gridDim.x;
+  // sequence of (unit, pass, chunk); units without passes skipped
+  struct Cur {
+    int64_t unit;
+    int p, kc;
+  };
+  auto first = [&](int64_t u) -> Cur {
+    while (u < u_end && qn[(int)(u & 3)] == 0) ++u;
+    return Cur{u < u_end ? u : nunits, 0, 0};
+  };
+  auto advance = [&](Cur& c) {
+    if (++c.kc < KC) return;
+    c.kc = 0;
+    if (++c.p < qn[(int)(c.unit & 3)]) return;
+    c = first(c.unit + 1);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kM2Stages; ++s) {
+      mbar_init(afull + s, kM2Build * 32);
+      mbar_init(bfull + s, 1);
+      mbar_init(sdone + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, kM2Epi * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kM2MmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_hold)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_hold;
+
+  if (warp == kM2MmaWarp) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      // F32 accumulate, F16 A / B, A MN-major (bit 15), B K-major, N, M = 128
+      const uint32_t idesc = (1u << 4) | (1u << 15) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kMmaM >> 4) << 24);
+      int s = 0;
+      unsigned ph = 0u;
+      int64_t npass = 0;  // passes started
+      for (Cur c = first(u_begin); c.unit < nunits; advance(c)) {
+        const int a = (int)(npass & 1);
+        if (c.kc == 0 && npass >= 2) mbar_wait(tempty + a, (unsigned)(((npass >> 1) - 1) & 1));  // epilogue of pass - 2
+        mbar_wait(afull + s, ph);
+        mbar_wait(bfull + s, ph);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(As + s * kM2AStage), b0 = smem_u32(Bs + s * kM2BStage);
+#pragma unroll
+        for (int k = 0; k < kM2K / 16; ++k)
+          umma_f16(tmem + 256 * a, umma_desc_mn128(a0 + 4096 * k), umma_desc_k128(b0 + 32 * k), idesc,
+                   (c.kc > 0 || k > 0) ? 1u : 0u);
+        umma_commit(sdone + s);
+        if (c.kc == KC - 1) {
+          umma_commit(tfull + a);
+          ++npass;
+        }
+        if (++s == kM2Stages) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kM2MmaWarp + 1) {
+    // ---------------- B loader
+    if (lane == 0) {
+      int s = 0;
+      unsigned ph = 0u;
+      bool warm = false;
+      for (Cur c = first(u_begin); c.unit < nunits; advance(c)) {
+        if (warm) mbar_wait(sdone + s, ph);
+        const int p = qf[(int)(c.unit & 3)] + c.p;
+        mbar_arrive_expect_tx(bfull + s, bbytes);
+        bulk_g2s_plain(Bs + s * kM2BStage, bimg + ((int64_t)p * KC + c.kc) * (bbytes / 16), bbytes, bfull + s);
+        if (++s == kM2Stages) {
+          s = 0;
+          if (warm) ph ^= 1u;
+          warm = true;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < kM2Build) {
+    // ---------------- builders: warp w, vertices 8 w .. 8 w + 7 of each chunk; lane t, images 4t..4t+3
+    const int t = lane;
+    // MN-major A: element (image m, vertex k) at (k/8) 2048 + (m/64) 1024 + (k%8) 128 +
+    // (((m%64)/8) ^ (k%8)) 16 + (m%8) 2; this lane's 4 images are 8 contiguous bytes
+    const uint32_t mb = (uint32_t)(t >> 4) * 1024u, mc = (uint32_t)((t & 15) >> 1), me = (uint32_t)(t & 1) * 8u;
+    int s = 0;
+    unsigned ph = 0u;
+    bool warm = false;
+    for (Cur c = first(u_begin); c.unit < nunits; advance(c)) {
+      if (warm) mbar_wait(sdone + s, ph);
+      const int o = (int)(c.unit & 3);
+      const int dc = (o & 1) ? -1 : 1, dr = (o & 2) ? -1 : 1;
+      const uint32_t rbit = dr > 0 ? 1u : 2u, cbit = dc > 0 ? 4u : 8u;
+      const uint32_t* px = (const uint32_t*)(pixT + (c.unit >> 2) * (int64_t)HW * 128) + t;  // [v][32 words]
+      uint8_t* as = As + s * kM2AStage;
+      // the warp's 8 vertices walked against dc: the column neighbour is the previous step
+      const int vlo = c.kc * kM2K + 8 * warp;
+      uint32_t Cp0 = 0u, Cp1 = 0u, Dp0 = 0u, Dp1 = 0u;
+      {  // the first step's column neighbour (v + dc of the walk start)
+        const int vs = dc > 0 ? vlo + 7 : vlo;
+        const int vn = vs + dc;
+        if (vn >= 0 && vn < HW) {
+          const uint32_t X = __ldg(px + (int64_t)vn * 32);
+          Cp0 = __byte_perm(X, 0, 0x4140);
+          Cp1 = __byte_perm(X, 0, 0x4342);
+          const int vr = vn + dr * W;
+          if (vr >= 0 && vr < HW) {
+            const uint32_t R = __ldg(px + (int64_t)vr * 32);
+            Dp0 = __byte_perm(R, 0, 0x4140);
+            Dp1 = __byte_perm(R, 0, 0x4342);
+          }
+        }
+      }
+#pragma unroll
+      for (int st = 0; st < 8; ++st) {
+        const int v = dc > 0 ? vlo + 7 - st : vlo + st;
+        uint32_t lo = 0u, hi = 0u;  // fp16 of images (4t, 4t+1) and (4t+2, 4t+3)
+        uint32_t A0 = 0u, A1 = 0u, R0 = 0u, R1 = 0u;
+        if (v < HW) {
+          const uint32_t f = __ldg(vflags + v);
+          const uint32_t X = __ldg(px + (int64_t)v * 32);
+          A0 = __byte_perm(X, 0, 0x4140);
+          A1 = __byte_perm(X, 0, 0x4342);
+          const bool hasr = (f & rbit) != 0, hasc = (f & cbit) != 0;
+          if (hasr) {
+            const uint32_t Rw = __ldg(px + (int64_t)(v + dr * W) * 32);
+            R0 = __byte_perm(Rw, 0, 0x4140);
+            R1 = __byte_perm(Rw, 0, 0x4342);
+          }
+          const uint32_t MC0 = hasc ? __vmaxu2(A0, Cp0) : 0u, MC1 = hasc ? __vmaxu2(A1, Cp1) : 0u;
+          const uint32_t MR0 = hasr ? __vmaxu2(A0, R0) : 0u, MR1 = hasr ? __vmaxu2(A1, R1) : 0u;
+          const uint32_t MD0 = (hasc && hasr) ? __vmaxu2(__vmaxu2(MC0, MR0), Dp0) : 0u;
+          const uint32_t MD1 = (hasc && hasr) ? __vmaxu2(__vmaxu2(MC1, MR1), Dp1) : 0u;
+          lo = A0 + MD0 + kMmaOff - MC0 - MR0;
+          hi = A1 + MD1 + kMmaOff - MC1 - MR1;
+        }
+        Cp0 = A0;
+        Cp1 = A1;
+        Dp0 = R0;
+        Dp1 = R1;
+        const uint32_t k = (uint32_t)(v - c.kc * kM2K);  // 0..63 within the chunk
+        const uint32_t r = k & 7u;
+        *(uint2*)(as + (k >> 3) * 2048u + mb + r * 128u + ((mc ^ r) << 4) + me) = make_uint2(lo, hi);
+      }
+      fence_async_smem();
+      mbar_arrive(afull + s);
+      if (++s == kM2Stages) {
+        s = 0;
+        if (warm) ph ^= 1u;
+        warm = true;
+      }
+    }
+  } else {
+    // ---------------- epilogue: warp e reads TMEM lanes 32 e .. +31 (images), 32 columns at a
+    // time, and stores them with TMA (box 32 bins x 1 direction x 32 images)
+    const int e = warp - kM2Build;
+    uint8_t* es = Es + e * 2 * kM2EStage;
+    int eb = 0;  // staging buffer
+    int64_t npass = 0;
+    for (Cur c = first(u_begin); c.unit < nunits;) {
+      const int o = (int)(c.unit & 3);
+      const int64_t img0 = (c.unit >> 2) * kMmaM + 32 * e;
+      for (int pp = 0; pp < qn[o]; ++pp) {
+        const int p = qf[o] + pp;
+        const int a = (int)(npass & 1);
+        mbar_wait(tfull + a, (unsigned)((npass >> 1) & 1));
+        tc_fence_after();
+        const int nd = tab[p * kMmaPassCols + 1];
+        for (int n0 = 0; n0 < N; n0 += 32) {
+          uint32_t r[32];
+          WECT_TMEM_LD32(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(256 * a + n0), r);
+          const int j = n0 / Tq, q0 = n0 - j * Tq;
+          const bool live = j < nd && q0 < T;
+          float4 f[8];
+          int dl = 0;
+          if (live) {
+            dl = tab[p * kMmaPassCols + 2 + j];
+            const float4* cf = (const float4*)(cfix + (int64_t)p * N + n0);
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4) f[k4] = __ldg(cf + k4);
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (!live) continue;
+          // the staging buffer's previous TMA store has read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          uint8_t* sb = es + eb * kM2EStage;
+          if (sizeof(OutT) == 4) {
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4) {
+              int4 v;
+              v.x = __float_as_int(__fadd_rn(__int_as_float(r[4 * k4 + 0]), f[k4].x)) - 0x4B400000;
+              v.y = __float_as_int(__fadd_rn(__int_as_float(r[4 * k4 + 1]), f[k4].y)) - 0x4B400000;
+              v.z = __float_as_int(__fadd_rn(__int_as_float(r[4 * k4 + 2]), f[k4].z)) - 0x4B400000;
+              v.w = __float_as_int(__fadd_rn(__int_as_float(r[4 * k4 + 3]), f[k4].w)) - 0x4B400000;
+              // row = lane (image), 16-byte chunk k4 swizzled by (lane & 7)
+              *(int4*)(sb + lane * 128 + ((k4 ^ (lane & 7)) << 4)) = v;
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&omap),
+                "r"(smem_u32(sb)), "r"(q0), "r"(dl), "r"((int)img0)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          eb ^= 1;
+        }
+        tc_fence_before();
+        mbar_arrive(tempty + a);
+        ++npass;
+      }
+      c = first(c.unit + 1);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kM2MmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -609,6 +978,92 @@ wect_status launch_mma2d(const uint8_t* img, int64_t B, int H, int W, const floa
     k_mma2d<long long><<<grid, kMmaThreads, smem, st>>>(img, B, H, W, T, Tq, N, KC, Dc, info, tab, bimg, cfix,
                                                         (long long*)out);
   }
+  count_launch();
+  timer.stop();
+  WECT_CUDA_TRY(cudaGetLastError());
+  return WECT_OK;
+}
+
+// ---- v2 host side
+static PFN_cuTensorMapEncodeTiled_v12000 m2_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// v2 needs int32 output that a TMA map can describe, and the B chunks within the scratch cap
+bool mma2_usable(void* out, int64_t B, int Dc, int T, wect_dtype odtype) {
+  return odtype == WECT_I32 && ((uintptr_t)out & 15) == 0 && ((int64_t)T * 4) % 16 == 0 && B <= 0xFFFFFFFFll &&
+         m2_encode() != nullptr;
+}
+
+size_t mma2_scratch_bytes(int HW, int Dc, int T, int64_t B) {
+  const int N = mma_n(T), KC = m2_kc(HW), dpp = mma_dpp(T);
+  const int npass_max = (Dc + dpp - 1) / dpp + 4;
+  const int64_t ntiles = (B + kMmaM - 1) / kMmaM;
+  return 256 + (size_t)Dc * HW * 2 + 16 + (size_t)Dc * T * 4 + 16 + (16 + 4 * Dc) * 4 + 16 +
+         (size_t)npass_max * kMmaPassCols * 4 + 1024 + (size_t)npass_max * KC * N * kM2K * 2 + 16 +
+         (size_t)npass_max * N * 4 + 256 + (size_t)ntiles * HW * 128 + 256 + (size_t)HW + 16;
+}
+
+wect_status launch_mma2(const uint8_t* img, int64_t B, int H, int W, const float* dirs, int d_begin, int Dc, int T,
+                        const GridParams* gp, void* scratch, void* out, cudaStream_t st, int num_sms) {
+  const int HW = H * W, N = mma_n(T), KC = m2_kc(HW), dpp = mma_dpp(T), Tq = mma_tq(T);
+  const int npass_max = (Dc + dpp - 1) / dpp + 4;
+  const int64_t ntiles = (B + kMmaM - 1) / kMmaM;
+  auto al = [](uintptr_t x, uintptr_t a) { return (x + a - 1) & ~(a - 1); };
+  uintptr_t cur = al((uintptr_t)scratch, 256);
+  uint16_t* vbin = (uint16_t*)cur;
+  cur = al(cur + (size_t)Dc * HW * 2, 16);
+  int* cum = (int*)cur;
+  cur = al(cur + (size_t)Dc * T * 4, 16);
+  int* qcount = (int*)cur;
+  int* info = qcount + 4;
+  int* qlist = qcount + 16;
+  cur = al(cur + (size_t)(16 + 4 * Dc) * 4, 16);
+  int* tab = (int*)cur;
+  cur = al(cur + (size_t)npass_max * kMmaPassCols * 4, 1024);
+  uint4* bimg = (uint4*)cur;
+  cur = al(cur + (size_t)npass_max * KC * N * kM2K * 2, 16);
+  float* cfix = (float*)cur;
+  cur = al(cur + (size_t)npass_max * N * 4, 256);
+  uint8_t* pixT = (uint8_t*)cur;
+  cur = al(cur + (size_t)ntiles * HW * 128, 256);
+  uint8_t* vflags = (uint8_t*)cur;
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)T, (cuuint64_t)Dc, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {(cuuint64_t)T * 4, (cuuint64_t)Dc * T * 4};
+    const cuuint32_t box[3] = {32u, 1u, 32u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = m2_encode()(&omap, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, out, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(WECT_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
+  WECT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 16 * sizeof(int), st));
+  k_mma_dirs<<<Dc, 256, (size_t)T * 4, st>>>(H, W, dirs, d_begin, Dc, gp, vbin, cum, qcount, qlist);
+  k_mma_passes<<<1, 32, 0, st>>>(qcount, qlist, Dc, dpp, tab, info);
+  k_mma2_bimg<<<npass_max * KC, 256, 0, st>>>(HW, T, Tq, N, KC, info, tab, vbin, cum, bimg, cfix);
+  k_mma2_pixt<<<dim3((unsigned)ntiles, (unsigned)((HW + 127) / 128)), 256, 0, st>>>(img, B, HW, pixT);
+  k_mma2_vflags<<<(HW + 255) / 256, 256, 0, st>>>(H, W, vflags);
+  count_launch(5);
+  WECT_CUDA_TRY(cudaGetLastError());
+  const size_t smem = m2_smem_bytes();
+  const int64_t nunits = 4 * ntiles;
+  const int grid = (int)(nunits < num_sms ? nunits : num_sms);
+  MainTimer timer(st);
+  WECT_CUDA_TRY(cudaFuncSetAttribute(k_mma2<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_mma2<int32_t><<<grid, kM2Threads, smem, st>>>(pixT, vflags, B, H, W, T, Tq, N, KC, info, tab, bimg, cfix, omap);
   count_launch();
   timer.stop();
   WECT_CUDA_TRY(cudaGetLastError());

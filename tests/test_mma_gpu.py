@@ -70,3 +70,16 @@ def test_mma_cfg2_batch_sampled():
         assert (out[idx] == oracle.wect_images(img[idx], dirs, T)).all()
     finally:
         del os.environ["WECT_IMAGES_MMA"]
+
+
+@pytest.mark.parametrize("H,W,B,D,T", [(28, 28, 150, 16, 128), (8, 12, 33, 9, 40), (28, 28, 300, 16, 128),
+                                       (12, 4, 130, 7, 64), (5, 16, 3, 33, 200)])
+def test_mma_v2_vs_O2(monkeypatch, H, W, B, D, T):
+    """The second contraction kernel (WECT_IMAGES_MMA=2: A written MN-major from per-tile
+    transposed pixels read through L1, 64-vertex SWIZZLE_128B chunks, TMEM double-buffered,
+    TMA-store epilogue of 128-byte rows), int32 output, bit-exact vs O2."""
+    monkeypatch.setenv("WECT_IMAGES_MMA", "2")
+    g = np.random.default_rng(H + W + B)
+    img = g.integers(0, 256, (B, H, W), dtype=np.uint8)
+    dirs = synth.directions_s1(D) if D % 2 else g.standard_normal((D, 2)).astype(np.float32)
+    assert (_run(img, dirs, T) == oracle.wect_images(img, dirs, T)).all()
