@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
   int* rbase = sh + Tp;
   int* totals = sh + 2 * Tp;
   uint16_t* vbin = (uint16_t*)(sh + 3 * Tp);
-  __shared__ int sh_split, sh_nl, sh_tot;
+  __shared__ int sh_split, sh_nl;
   // rows in record j of a bin of c rows
   auto counts_total_rows = [&](int q, int j) {
     const int c = totals[q] - j * kRecRows;
@@ -196,7 +196,6 @@ __global__ void __launch_bounds__(256) k_sort2d(int H, int W, const float* __res
       const int nl = sb < Tp ? rbase[sb] : tot;
       split[dl] = make_int4(nl, tot - nl, sb, 0);
       sh_nl = nl;
-      sh_tot = tot;
     }
     __syncwarp();
     // records of the upper program run from the top bin down: bin q >= sb starts at
