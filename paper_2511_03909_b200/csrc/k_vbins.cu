@@ -143,7 +143,12 @@ __device__ __forceinline__ void vb_batch(const int* rec, int nb, const uint32_t*
 #pragma unroll
     for (int u = 0; u < kVbU; ++u)
 #pragma unroll
-      for (int t = 0; t < AR; ++t) x[u][t] = __ldg(vbl + (int64_t)r[u][t] * 32);
+      for (int t = 0; t < AR; ++t)
+#ifdef WECT_VB_NOGATHER  // A/B experiment only: bins from the id, no VB row loads (wrong results)
+        x[u][t] = ((uint32_t)r[u][t] & 0x1FFu) * 0x10001u;
+#else
+        x[u][t] = __ldg(vbl + (int64_t)r[u][t] * 32);
+#endif
 #pragma unroll
     for (int u = 0; u < kVbU; ++u) {
       uint32_t m2 = x[u][0];
@@ -161,8 +166,14 @@ __device__ __forceinline__ void vb_batch(const int* rec, int nb, const uint32_t*
         hist_add(hl + lo * 64, w);
         hist_add(hl + hi * 64 + 32, w);
       } else {
-        red_shared(hsa + lo * 256u, wi);
-        red_shared(hsa + hi * 256u + 128u, wi);
+#ifdef WECT_VB_NOATOM  // A/B experiment only: every load and max, no atomics (bins never 0xFFFF)
+        if (m2 == 0xFFFFFFFFu) {
+#else
+        {
+#endif
+          red_shared(hsa + lo * 256u, wi);
+          red_shared(hsa + hi * 256u + 128u, wi);
+        }
       }
     }
   }
