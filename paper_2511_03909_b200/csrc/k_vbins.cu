@@ -27,15 +27,6 @@ struct VecN {
   float v[N];
 };
 
-// binary64 height of one vertex in one direction (axis order), alpha64 (reading A1)
-template <int N>
-__device__ __noinline__ int vertex_repair(const VecN<N> x, const VecN<N> s, const GridParams* gp) {
-  double h = __dmul_rn((double)x.v[0], (double)s.v[0]);
-  for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x.v[i], (double)s.v[i]));
-  note_repair();
-  return alpha64(h, *gp);
-}
-
 // grid: blocks over vertices; lanes = direction pairs of the tile (inactive pairs of the
 // last tile compute a harmless bin of direction 0 that nobody reads); each warp stages 32
 // vertices' coordinates (lane-parallel), then writes one 128-byte VB row per vertex.
@@ -61,25 +52,46 @@ __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords,
     for (int t = lane; t < nv * N; t += 32) x[t] = __ldg(coords + base * N + t);
     __syncwarp();
     uint32_t* row = vb + base * 32 + lane;
-#pragma unroll 2
-    for (int j = 0; j < nv; ++j) {
-      VecN<N> xv;
-#pragma unroll
-      for (int i = 0; i < N; ++i) xv.v[i] = x[j * N + i];
-      float ha = xv.v[0] * sa.v[0], hb = xv.v[0] * sb.v[0];
+    // fp32 bins of vertex j (both directions) and whether either lies within tau of an edge
+    auto bins32 = [&](int j, int& ba, int& bb) -> uint32_t {
+      float ha = x[j * N] * sa.v[0], hb = x[j * N] * sb.v[0];
 #pragma unroll
       for (int i = 1; i < N; ++i) {
-        ha = fmaf(xv.v[i], sa.v[i], ha);
-        hb = fmaf(xv.v[i], sb.v[i], hb);
+        ha = fmaf(x[j * N + i], sa.v[i], ha);
+        hb = fmaf(x[j * N + i], sb.v[i], hb);
       }
       const float ua = fmaf(ha, g.A, g.B), ub = fmaf(hb, g.A, g.B);
-      int ba = max(0, min(__float2int_ru(ua), g.T - 1)), bb = max(0, min(__float2int_ru(ub), g.T - 1));
-      const bool na = fabsf(ua - rintf(ua)) < tau, nb = fabsf(ub - rintf(ub)) < tau;
-      if (__builtin_expect(na || nb, 0)) {
-        if (na) ba = vertex_repair<N>(xv, sa, gp);
-        if (nb) bb = vertex_repair<N>(xv, sb, gp);
-      }
+      ba = max(0, min(__float2int_ru(ua), g.T - 1));
+      bb = max(0, min(__float2int_ru(ub), g.T - 1));
+      return (fabsf(ua - rintf(ua)) < tau ? 1u : 0u) | (fabsf(ub - rintf(ub)) < tau ? 2u : 0u);
+    };
+    // Near-edge vertices are only flagged in the loop (bit j) and repaired after it, in a
+    // warp-uniform loop with the binary64 path inlined.  A divergent repair call inside the
+    // loop never reconverged: the warp ran the rest of the kernel as two halves, every row
+    // computed twice (ncu r02_k_vbins_cfg4: 1.5-2x the warp instructions).
+    uint32_t near = 0;
+#pragma unroll 2
+    for (int j = 0; j < nv; ++j) {
+      int ba, bb;
+      near |= (bins32(j, ba, bb) ? 1u : 0u) << j;
       row[(int64_t)j * 32] = (uint32_t)ba | ((uint32_t)bb << 16);
+    }
+    while (__any_sync(0xffffffffu, near != 0)) {
+      const bool act = near != 0;
+      const int j = act ? __ffs(near) - 1 : 0;
+      near &= near - 1;
+      int ba, bb;
+      const uint32_t f = act ? bins32(j, ba, bb) : 0u;
+      double ha = __dmul_rn((double)x[j * N], (double)sa.v[0]), hb = __dmul_rn((double)x[j * N], (double)sb.v[0]);
+#pragma unroll
+      for (int i = 1; i < N; ++i) {
+        ha = __dadd_rn(ha, __dmul_rn((double)x[j * N + i], (double)sa.v[i]));
+        hb = __dadd_rn(hb, __dmul_rn((double)x[j * N + i], (double)sb.v[i]));
+      }
+      const int ra = alpha64(ha, g), rb = alpha64(hb, g);
+      const unsigned ca = __ballot_sync(0xffffffffu, f & 1u), cb = __ballot_sync(0xffffffffu, f & 2u);
+      if (lane == 0 && (ca | cb)) atomicAdd(&g_repair_count, (unsigned long long)(__popc(ca) + __popc(cb)));
+      if (act) row[(int64_t)j * 32] = (uint32_t)(f & 1u ? ra : ba) | ((uint32_t)(f & 2u ? rb : bb) << 16);
     }
     __syncwarp();
   }
