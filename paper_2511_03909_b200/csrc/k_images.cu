@@ -173,12 +173,28 @@ __global__ void __launch_bounds__(256) k_grid_cw(const uint8_t* __restrict__ img
 constexpr int kSegVox = 128;     // voxels per staged row segment
 constexpr int kSegStride = 136;  // int16 per staged octant row (68 words = 4 mod 32: conflict-free)
 
-__device__ __noinline__ int grid_repair(float cx, float cy, float cz, float s0, float s1, float s2, int nd,
-                                        const GridParams* gp) {
+// Inlined and called from warp-uniform loops only: a divergent (noinline) repair call left
+// warps split for the rest of the kernel (measured in k_vbins: 1.5x the instructions).
+__device__ __forceinline__ int grid_repair(float cx, float cy, float cz, float s0, float s1, float s2, int nd,
+                                           const GridParams* gp) {
   double h64 = __dadd_rn(__dmul_rn((double)cx, (double)s0), __dmul_rn((double)cy, (double)s1));
   if (nd == 3) h64 = __dadd_rn(h64, __dmul_rn((double)cz, (double)s2));
-  note_repair();
   return alpha64(h64, *gp);
+}
+// repair the voxels flagged in nm (bit h: voxel x + h of this lane's row) in a warp-uniform
+// loop; out[h] = f(binary64 bin of voxel h)
+template <typename F>
+__device__ __forceinline__ void grid_repair_mask(uint32_t nm, const float* axc0, int x, float cy, float cz,
+                                                 const float* s, int nd, const GridParams* gp, int lane, F&& set) {
+  while (__any_sync(0xffffffffu, nm != 0)) {
+    const bool act = nm != 0;
+    const int hh = act ? __ffs(nm) - 1 : 0;
+    nm &= nm - 1;
+    const int r = grid_repair(axc0[x + hh], cy, cz, s[0], s[1], s[2], nd, gp);
+    const unsigned c = __ballot_sync(0xffffffffu, act);
+    if (lane == 0) atomicAdd(&g_repair_count, (unsigned long long)__popc(c));
+    if (act) set(hh, r);
+  }
 }
 
 // predicated shared-memory add (no branch, no reconvergence barrier)
@@ -376,13 +392,18 @@ __global__ void __launch_bounds__(256, 3) k_grid_hist(const int16_t* __restrict_
           }
           // warp vote: a uniform branch, no reconvergence barrier in the common case
           if (__builtin_expect(__any_sync(0xffffffffu, emin < tau || emax > 1.f - tau), 0)) {
+            uint32_t nm = 0;
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
               const float u = fmaf(xf + (float)h, a0, U0);
               const float e = (__fadd_ru(u, kMagic) - kMagic) - u;
-              if ((e < tau || e > 1.f - tau) && h < nvalid)  // padding voxels need no repair
-                adr[h] = hlane + 128u * (uint32_t)grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
+              nm |= ((e < tau || e > 1.f - tau) && h < nvalid ? 1u : 0u) << h;  // padding needs no repair
             }
+            grid_repair_mask(nm, axc[0], x0 + xi, cy, cz, s, ND, gp, lane, [&](int hh, int r) {
+#pragma unroll
+              for (int h = 0; h < 8; ++h)
+                if (h == hh) adr[h] = hlane + 128u * (uint32_t)r;
+            });
           }
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
@@ -404,12 +425,16 @@ __global__ void __launch_bounds__(256, 3) k_grid_hist(const int16_t* __restrict_
             dist[h] = fabsf(u - rintf(u));
             dmin = fminf(dmin, dist[h]);
           }
-          if (__builtin_expect(dmin < tau, 0)) {  // some voxel of the group sits near a bin edge
+          if (__builtin_expect(__any_sync(0xffffffffu, dmin < tau), 0)) {  // a voxel near a bin edge
             const int nvalid = nx - xi;  // padding voxels need no repair
+            uint32_t nm = 0;
 #pragma unroll
-            for (int h = 0; h < 8; ++h)
-              if (dist[h] < tau && h < nvalid)
-                bin[h] = grid_repair(axc[0][x0 + xi + h], cy, cz, s[0], s[1], s[2], ND, gp);
+            for (int h = 0; h < 8; ++h) nm |= (dist[h] < tau && h < nvalid ? 1u : 0u) << h;
+            grid_repair_mask(nm, axc[0], x0 + xi, cy, cz, s, ND, gp, lane, [&](int hh, int r) {
+#pragma unroll
+              for (int h = 0; h < 8; ++h)
+                if (h == hh) bin[h] = r;
+            });
           }
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
