@@ -26,35 +26,85 @@ __device__ unsigned long long g_repair_count = 0;
 // R1 = max_v sum_i |x_vi| (for the guard).  pass 2 recomputes in binary64 every vertex
 // whose fp32 max is within 2 err of M32 (err bounds |h32 - h64|), so the exact M64 =
 // max |h64| is found (reading A2).
+constexpr int kVmaxChunk = 4096;  // directions per shared-memory chunk of k_vmax_pass1 (<= 128 KB)
+
 template <int N>
 __global__ void __launch_bounds__(256) k_vmax_pass1(const float* __restrict__ coords, int64_t k0,
                                                     const float* __restrict__ dirs, int D, float* __restrict__ vmax,
                                                     unsigned int* __restrict__ m32_bits, unsigned int* __restrict__ r1_bits,
                                                     unsigned int* __restrict__ smax_bits) {
-  extern __shared__ float sdir[];  // [D][N]
-  float sm = 0.f;
-  for (int i = threadIdx.x; i < D * N; i += blockDim.x) { sdir[i] = dirs[i]; sm = fmaxf(sm, fabsf(dirs[i])); }
+  extern __shared__ float sdir[];  // [KC][NP]: N <= 4 zero-padded to float4 rows (one LDS.128 per direction)
+  constexpr int NP = N <= 4 ? 4 : N;
+  constexpr int KC = kVmaxChunk;     // directions per shared-memory chunk
+  float sm = 0.f, bm = 0.f, br = 0.f;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int p0 = 0; p0 < D; p0 += KC) {
+    const int dc = (D - p0) < KC ? (D - p0) : KC;
+    const bool first = p0 == 0;
+    __syncthreads();  // the previous chunk is consumed
+    for (int i = threadIdx.x; i < dc * NP; i += blockDim.x) {
+      const int p = i / NP, k = i - p * NP;
+      const float d = k < N ? dirs[(int64_t)(p0 + p) * N + k] : 0.f;
+      sdir[i] = d;
+      sm = fmaxf(sm, fabsf(d));
+    }
+    __syncthreads();
+    if constexpr (N <= 4) {
+      // two vertices per thread share every direction load
+      for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < k0; v += 2 * nt) {
+        const int64_t v1 = v + nt;
+        const bool has1 = v1 < k0;
+        float x0[N], x1[N];
+        float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          x0[i] = coords[v * N + i];
+          x1[i] = has1 ? coords[v1 * N + i] : x0[i];
+          r0 += fabsf(x0[i]);
+          r1 += fabsf(x1[i]);
+        }
+        float m0 = first ? 0.f : vmax[v], m1 = (first || !has1) ? 0.f : vmax[v1];
+        const float4* sd4 = (const float4*)sdir;
+#pragma unroll 4
+        for (int p = 0; p < dc; ++p) {
+          const float4 d = sd4[p];
+          const float dv[4] = {d.x, d.y, d.z, d.w};
+          float h0 = x0[0] * dv[0], h1 = x1[0] * dv[0];
+#pragma unroll
+          for (int i = 1; i < N; ++i) {
+            h0 = fmaf(x0[i], dv[i], h0);
+            h1 = fmaf(x1[i], dv[i], h1);
+          }
+          m0 = fmaxf(m0, fabsf(h0));
+          m1 = fmaxf(m1, fabsf(h1));
+        }
+        vmax[v] = m0;
+        if (has1) vmax[v1] = m1;
+        bm = fmaxf(bm, has1 ? fmaxf(m0, m1) : m0);
+        br = fmaxf(br, fmaxf(r0, r1));
+      }
+    } else {
+      for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < k0; v += nt) {
+        float x[N];
+        float r1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) { x[i] = coords[v * N + i]; r1 += fabsf(x[i]); }
+        float m = first ? 0.f : vmax[v];
+        for (int p = 0; p < dc; ++p) {
+          float h = x[0] * sdir[p * N];
+#pragma unroll
+          for (int i = 1; i < N; ++i) h = fmaf(x[i], sdir[p * N + i], h);
+          m = fmaxf(m, fabsf(h));
+        }
+        vmax[v] = m;
+        bm = fmaxf(bm, m);
+        br = fmaxf(br, r1);
+      }
+    }
+  }
   if (blockIdx.x == 0) {
     for (int o = 16; o; o >>= 1) sm = fmaxf(sm, __shfl_xor_sync(0xffffffffu, sm, o));
     if ((threadIdx.x & 31) == 0) atomicMax(smax_bits, __float_as_uint(sm));
-  }
-  __syncthreads();
-  float bm = 0.f, br = 0.f;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < k0; v += (int64_t)gridDim.x * blockDim.x) {
-    float x[N];
-    float r1 = 0.f;
-#pragma unroll
-    for (int i = 0; i < N; ++i) { x[i] = coords[v * N + i]; r1 += fabsf(x[i]); }
-    float m = 0.f;
-    for (int p = 0; p < D; ++p) {
-      float h = x[0] * sdir[p * N];
-#pragma unroll
-      for (int i = 1; i < N; ++i) h = fmaf(x[i], sdir[p * N + i], h);
-      m = fmaxf(m, fabsf(h));
-    }
-    vmax[v] = m;
-    bm = fmaxf(bm, m);
-    br = fmaxf(br, r1);
   }
   for (int o = 16; o; o >>= 1) {
     bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
@@ -417,7 +467,7 @@ static wect_status launch_vmax_n(const float* coords, int64_t k0, const float* d
   int blocks = (int)((k0 + 255) / 256);
   if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (blocks < 1) blocks = 1;
-  const size_t smem = (size_t)D * N * sizeof(float);
+  const size_t smem = (size_t)(D < kVmaxChunk ? D : kVmaxChunk) * (N <= 4 ? 4 : N) * sizeof(float);
   if (smem > 48 * 1024) WECT_CUDA_TRY(cudaFuncSetAttribute(k_vmax_pass1<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_vmax_pass1<N><<<blocks, 256, smem, st>>>(coords, k0, dirs, D, vmax, m32, r1, smax); count_launch();
   WECT_CUDA_TRY(cudaGetLastError());
