@@ -61,29 +61,10 @@ __device__ __forceinline__ const float* opaque(const float* p) {
 }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kStreamConsumers)); }
 
-__device__ __noinline__ int stream_ecf_repair(float hmax, const GridParams* gp) {
-  note_repair();
-  return alpha64((double)hmax, *gp);  // filter values are exact in binary64
-}
-
 template <int AR>
 struct CellIds {
   int v[AR];
 };
-
-template <int N, int AR>
-__device__ __noinline__ int stream_wect_repair(const CellIds<AR> ids, const float* __restrict__ coords,
-                                               const float* s, const GridParams* gp) {
-  double hm = -DBL_MAX;
-  for (int t = 0; t < AR; ++t) {
-    const float* x = coords + (int64_t)ids.v[t] * N;
-    double h = __dmul_rn((double)x[0], (double)s[0]);
-    for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x[i], (double)s[i]));
-    hm = fmax(hm, h);
-  }
-  note_repair();
-  return alpha64(hm, *gp);
-}
 
 template <int MODE, int N, bool FLOATW>
 struct StreamCtx {
@@ -151,10 +132,19 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
         dist[k] = fabsf(uu - rintf(uu));
         dmin = fminf(dmin, dist[k]);
       }
-      if (__builtin_expect(dmin < c.tau, 0)) {  // some cell of the group sits near a bin edge
+      // some cell of the group sits near a bin edge: warp-uniform repair, binary64 inlined
+      // (a divergent repair call would leave the warp split)
+      if (__builtin_expect(__any_sync(0xffffffffu, dmin < c.tau), 0)) {
 #pragma unroll
-        for (int k = 0; k < KG; ++k)
-          if (dist[k] < c.tau) bin[k] = stream_ecf_repair(hm[k], c.gp);
+        for (int k = 0; k < KG; ++k) {
+          const bool nk = dist[k] < c.tau;
+          const unsigned bal = __ballot_sync(0xffffffffu, nk);
+          if (bal) {
+            const int r = alpha64((double)hm[k], c.g);  // filter values are exact in binary64
+            if (nk) bin[k] = r;
+            if (lane == 0) atomicAdd(&g_repair_count, (unsigned long long)__popc(bal));
+          }
+        }
       }
       if (!FLOATW && (c.direct || udirect)) {
 #pragma unroll
@@ -197,15 +187,25 @@ __device__ __forceinline__ void stream_group(const StreamCtx<MODE, N, FLOATW>& c
         dist[k] = fabsf(uu - rintf(uu));
         dmin = fminf(dmin, dist[k]);
       }
-      if (__builtin_expect(dmin < c.tau, 0)) {
+      if (__builtin_expect(__any_sync(0xffffffffu, dmin < c.tau), 0)) {  // warp-uniform, inlined
 #pragma unroll
-        for (int k = 0; k < KG; ++k)
-          if (dist[k] < c.tau) {
-            CellIds<AR> ids;
+        for (int k = 0; k < KG; ++k) {
+          const bool nk = dist[k] < c.tau;
+          const unsigned bal = __ballot_sync(0xffffffffu, nk);
+          if (bal) {
+            double hm64 = -DBL_MAX;
 #pragma unroll
-            for (int t = 0; t < AR; ++t) ids.v[t] = v[k][t];
-            bin[k] = stream_wect_repair<N, AR>(ids, c.coords, s, c.gp);
+            for (int t = 0; t < AR; ++t) {
+              double h = __dmul_rn((double)x[k][t * N], (double)sv[0]);
+#pragma unroll
+              for (int i = 1; i < N; ++i) h = __dadd_rn(h, __dmul_rn((double)x[k][t * N + i], (double)sv[i]));
+              hm64 = fmax(hm64, h);
+            }
+            const int r = alpha64(hm64, c.g);
+            if (nk) bin[k] = r;
+            if (lane == 0) atomicAdd(&g_repair_count, (unsigned long long)__popc(bal));
           }
+        }
       }
       if (!FLOATW && (c.direct || udirect)) {
 #pragma unroll
