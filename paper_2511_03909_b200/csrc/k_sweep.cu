@@ -9,16 +9,17 @@
 // s_k > 0), so all cells designating vertex v sum into one combined weight cw_o(v)
 // (o = quadrant of s, |cw| <= 255) and land in bin(v).
 //
-// k_sweep2d: a persistent CTA (16 warps, one per SM) takes 64 images at a time, stages
+// k_sweep2d: a persistent CTA (32 warps, one CTA per SM) takes 64 images at a time, stages
 // their pixels transposed, builds the quadrant's cw table in shared memory -- one 128-byte
 // row per vertex, word j = images (j, j+32) as a signed packed pair cw_j + cw_{j+32} 2^16 --
-// and each warp sweeps one direction: for every bin, its records' rows are gathered
-// (one LDS per row: every lane reads its own word of the same row) and summed, the sum is
-// unpacked onto two int32 running totals (images lane, lane+32).  The running total after
-// bin q IS the cumulative sum of the difference histogram (Alg. 1 lines 4-11):
-// no atomics, no separate scan, exact int32.  Bins are unrolled by output chunk (16 int32
-// / 8 int64 bins = 64 bytes per image), so every bin's total lands in a register; a chunk
-// goes to a per-warp 64-image x 64-byte shared stage (64B-swizzled: conflict-free
+// and two warps sweep each direction (one the bins below its split upwards, one the bins
+// above it downwards, emitting chi - rows above): for every bin, its records' rows are
+// gathered (one LDS per row: every lane reads its own word of the same row) and summed, the
+// sum is unpacked onto two int32 running totals (images lane, lane+32).  The running total
+// after bin q IS the cumulative sum of the difference histogram (Alg. 1 lines 4-11,
+// P:654-687): no atomics, no separate scan, exact int32.  Bins are unrolled by output chunk
+// (8 int32 / 4 int64 bins = 32 bytes per image), so every bin's total lands in a register; a
+// chunk goes to a per-warp 64-image x 32-byte shared stage (32B-swizzled: conflict-free
 // STS.128) and out to HBM with one TMA tensor store (cp.async.bulk.tensor), which takes
 // the strided [B, D, T] writes off the load/store pipe.
 #include <cuda.h>
@@ -43,7 +44,7 @@ constexpr int kRingBytes = kRingRecs * 32;  // 1 KB: halves at byte 0 and 512 (r
 constexpr int kSweepMaxHW = 1024;
 
 __host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
-// bins per output chunk for an output element of osz bytes (64-byte image rows)
+// bins per output chunk for an output element of osz bytes (32-byte image rows)
 __host__ __device__ constexpr int chunk_bins(int osz) { return kStageRow / osz; }
 // 32-byte records per direction: one per bin at least, + one per 15 vertices, + the prefetch pad
 __host__ __device__ constexpr int sweep_rec_stride(int HW, int Tp) { return Tp + (HW + kRecRows - 1) / kRecRows + 8; }
