@@ -31,10 +31,11 @@ struct VecN {
 // last tile compute a harmless bin of direction 0 that nobody reads); each warp stages 32
 // vertices' coordinates (lane-parallel), then writes one 128-byte VB row per vertex.
 template <int N>
-__global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords, int64_t k0,
+__global__ void __launch_bounds__(256, 4) k_vbins(const float* __restrict__ coords, int64_t k0,
                                                const float* __restrict__ dirs, int p0, int np,
                                                const GridParams* __restrict__ gp, uint32_t* __restrict__ vb) {
-  __shared__ float xs[8][32 * N];
+  constexpr int XS = N <= 4 ? 4 : N;  // staged floats per vertex (N <= 4: one LDS.128 per vertex)
+  __shared__ __align__(16) float xs[8][32 * XS];
   const GridParams g = *gp;
   const float tau = g.fp32_only ? -1.f : g.tau;  // fp32-only: the guard never fires
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -49,16 +50,27 @@ __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords,
   const int64_t nwarps = (int64_t)gridDim.x * 8;
   for (int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 32; base < k0; base += nwarps * 32) {
     const int nv = (k0 - base) < 32 ? (int)(k0 - base) : 32;
-    for (int t = lane; t < nv * N; t += 32) x[t] = __ldg(coords + base * N + t);
+    for (int t = lane; t < nv * N; t += 32) {
+      const int vv = t / N;
+      x[vv * XS + (t - vv * N)] = __ldg(coords + base * N + t);
+    }
     __syncwarp();
     uint32_t* row = vb + base * 32 + lane;
     // fp32 bins of vertex j (both directions) and whether either lies within tau of an edge
     auto bins32 = [&](int j, int& ba, int& bb) -> uint32_t {
-      float ha = x[j * N] * sa.v[0], hb = x[j * N] * sb.v[0];
+      float xv[XS];
+      if constexpr (XS == 4) {
+        const float4 q = *(const float4*)(x + j * 4);
+        xv[0] = q.x; xv[1] = q.y; xv[2] = q.z; xv[3] = q.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) xv[i] = x[j * XS + i];
+      }
+      float ha = xv[0] * sa.v[0], hb = xv[0] * sb.v[0];
 #pragma unroll
       for (int i = 1; i < N; ++i) {
-        ha = fmaf(x[j * N + i], sa.v[i], ha);
-        hb = fmaf(x[j * N + i], sb.v[i], hb);
+        ha = fmaf(xv[i], sa.v[i], ha);
+        hb = fmaf(xv[i], sb.v[i], hb);
       }
       const float ua = fmaf(ha, g.A, g.B), ub = fmaf(hb, g.A, g.B);
       ba = max(0, min(__float2int_ru(ua), g.T - 1));
@@ -70,11 +82,17 @@ __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords,
     // loop never reconverged: the warp ran the rest of the kernel as two halves, every row
     // computed twice (ncu r02_k_vbins_cfg4: 1.5-2x the warp instructions).
     uint32_t near = 0;
-#pragma unroll 2
-    for (int j = 0; j < nv; ++j) {
+    auto body = [&](int j) {
       int ba, bb;
-      near |= (bins32(j, ba, bb) ? 1u : 0u) << j;
-      row[(int64_t)j * 32] = (uint32_t)ba | ((uint32_t)bb << 16);
+      if (bins32(j, ba, bb)) near |= 1u << j;
+      row[j * 32] = (uint32_t)ba | ((uint32_t)bb << 16);
+    };
+    if (nv == 32) {  // fully unrolled: immediate shared / global offsets and flag bits
+#pragma unroll
+      for (int j = 0; j < 32; ++j) body(j);
+    } else {
+#pragma unroll 2
+      for (int j = 0; j < nv; ++j) body(j);
     }
     while (__any_sync(0xffffffffu, near != 0)) {
       const bool act = near != 0;
@@ -82,16 +100,16 @@ __global__ void __launch_bounds__(256) k_vbins(const float* __restrict__ coords,
       near &= near - 1;
       int ba, bb;
       const uint32_t f = act ? bins32(j, ba, bb) : 0u;
-      double ha = __dmul_rn((double)x[j * N], (double)sa.v[0]), hb = __dmul_rn((double)x[j * N], (double)sb.v[0]);
+      double ha = __dmul_rn((double)x[j * XS], (double)sa.v[0]), hb = __dmul_rn((double)x[j * XS], (double)sb.v[0]);
 #pragma unroll
       for (int i = 1; i < N; ++i) {
-        ha = __dadd_rn(ha, __dmul_rn((double)x[j * N + i], (double)sa.v[i]));
-        hb = __dadd_rn(hb, __dmul_rn((double)x[j * N + i], (double)sb.v[i]));
+        ha = __dadd_rn(ha, __dmul_rn((double)x[j * XS + i], (double)sa.v[i]));
+        hb = __dadd_rn(hb, __dmul_rn((double)x[j * XS + i], (double)sb.v[i]));
       }
       const int ra = alpha64(ha, g), rb = alpha64(hb, g);
       const unsigned ca = __ballot_sync(0xffffffffu, f & 1u), cb = __ballot_sync(0xffffffffu, f & 2u);
       if (lane == 0 && (ca | cb)) atomicAdd(&g_repair_count, (unsigned long long)(__popc(ca) + __popc(cb)));
-      if (act) row[(int64_t)j * 32] = (uint32_t)(f & 1u ? ra : ba) | ((uint32_t)(f & 2u ? rb : bb) << 16);
+      if (act) row[j * 32] = (uint32_t)(f & 1u ? ra : ba) | ((uint32_t)(f & 2u ? rb : bb) << 16);
     }
     __syncwarp();
   }
